@@ -1,0 +1,130 @@
+/*
+ * mfwq.h -- C-ABI of the B200-native MF-WQ hot path (libmfwq.so).
+ *
+ * Drop-in boundary for the reference's Python operator API (igamf 0.1.0,
+ * /root/reference/pkg/src/igamf).  Plain pointers and sizes only; device
+ * buffers are fp64 CUDA pointers on the current device, streams are
+ * cudaStream_t passed as void*.  Every function returns MFWQ_OK or an error
+ * code; mfwq_last_error() gives the message (thread-local).  Error codes map
+ * onto the reference's exception types (see MFWQ_E_*).
+ *
+ * Reference interfaces replaced (file:line in pkg/src/igamf):
+ *   mfwq_rule1d_*          build_wq_rule / wq_points / wq_weights      wq.py:62-164
+ *                          collocation_matrix                          splines.py:165-192
+ *   mfwq_univariate_km     univariate_parametric_matrices              solvers.py:48-62
+ *   mfwq_stiffness_create  StiffnessOperator.__init__ / setup_stiffness operators.py:138-163, 227
+ *   mfwq_stiffness_set_*   _eval_stiffness_coeffs                      operators.py:64-84
+ *   mfwq_stiffness_apply   StiffnessOperator.apply                     operators.py:185-204
+ *   mfwq_stiffness_flops   CostMeter count of one apply                kron.py:90-96, operators.py:199-203
+ *   mfwq_fd_create         FDPreconditioner.__init__                   solvers.py:72-101
+ *   mfwq_fd_apply          FDPreconditioner.apply                      solvers.py:107-115
+ *   mfwq_pcg_solve         cg (device-resident loop)                   solvers.py:137-173
+ */
+#ifndef MFWQ_H_
+#define MFWQ_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define MFWQ_OK 0
+#define MFWQ_E_VALUE 1        /* ValueError                 */
+#define MFWQ_E_WQ 2           /* WQConstructionError        (wq.py:29-39)        */
+#define MFWQ_E_DEGENERATE 3   /* DegenerateGeometryError    (operators.py:25-31) */
+#define MFWQ_E_EIGEN 4        /* EigenSolveError            (solvers.py:28)      */
+#define MFWQ_E_INDEFINITE 5   /* IndefiniteOperatorError    (solvers.py:24)      */
+#define MFWQ_E_CUDA 6         /* CUDA runtime failure                            */
+#define MFWQ_E_NOTIMPL 7      /* NotImplementedError                             */
+#define MFWQ_E_INTERNAL 8
+
+/* geometry kinds for mfwq_stiffness_set_geometry (geometry.py:47-96) */
+#define MFWQ_GEOM_IDENTITY 0
+#define MFWQ_GEOM_RING 1      /* quarter_ring_map (analytic polar map)           */
+#define MFWQ_GEOM_AFFINE 2    /* affine_map: J = A (row-major 3x3)               */
+#define MFWQ_GEOM_JACOBIAN 3  /* caller-supplied device Jacobians, (Nq,3,3)      */
+
+const char* mfwq_last_error(void);
+int mfwq_version(void);
+
+/* ---------------- 1D weighted-quadrature rule (host) ---------------- */
+typedef struct mfwq_rule1d_s* mfwq_rule1d_t;
+/* knots: open knot vector of degree p on [0,1] (splines.py:16-49) */
+int mfwq_rule1d_build(int p, int nknots, const double* knots, mfwq_rule1d_t* out);
+/* npts, nfun, boundary extra used, nnz[6] of W00,W01,W10,W11 (nfun x npts), B0,B1 (npts x nfun) */
+int mfwq_rule1d_sizes(mfwq_rule1d_t r, int* npts, int* nfun, int* extra, int* nnz6);
+/* copy out points and the six CSR matrices (caller-allocated, sizes from _sizes) */
+int mfwq_rule1d_export(mfwq_rule1d_t r, double* pts, int* const* indptr6, int* const* indices6,
+                       double* const* data6);
+void mfwq_rule1d_destroy(mfwq_rule1d_t r);
+/* interior (n x n, n = nfun-2) exact 1D stiffness K and mass M, row-major */
+int mfwq_univariate_km(int p, int nknots, const double* knots, double* K, double* M);
+
+/* ---------------- MF-WQ stiffness operator (device) ---------------- */
+typedef struct mfwq_stiffness_s* mfwq_stiffness_t;
+typedef struct {
+  int p[3];
+  int nknots[3];
+  const double* knots[3];
+  int npts[3];
+  const double* pts[3];
+  /* per direction l, the rule's full factors in CSR (host), index l*6 + k with
+     k = 0..3: W00,W01,W10,W11 (nfun x npts), k = 4,5: B0,B1 (npts x nfun) */
+  const int* indptr[18];
+  const int* indices[18];
+  const double* data[18];
+} mfwq_stiffness_desc;
+
+int mfwq_stiffness_create(const mfwq_stiffness_desc* d, mfwq_stiffness_t* out);
+/* kind: MFWQ_GEOM_*; affine9: row-major A for AFFINE; K9: constant diffusion
+   (NULL = identity); J_dev: device (Nq,3,3) for JACOBIAN; Kfield_dev: device
+   (Nq,3,3) per-point diffusion or NULL.  Raises MFWQ_E_DEGENERATE if det J <= 0. */
+int mfwq_stiffness_set_geometry(mfwq_stiffness_t h, int kind, const double* affine9, const double* K9,
+                                const double* J_dev, const double* Kfield_dev, void* stream);
+/* six device grids (a<=b order 00,01,02,11,12,22), each (m3,m2,m1) contiguous */
+int mfwq_stiffness_set_coeffs(mfwq_stiffness_t h, const double* const* grids6_dev, void* stream);
+int mfwq_stiffness_get_coeff(mfwq_stiffness_t h, int key, double* out_dev, void* stream);
+/* sizes: n[3], m[3], N, Nq */
+int mfwq_stiffness_sizes(mfwq_stiffness_t h, int* n3, int* m3, long long* N, long long* Nq);
+/* y = K x  (device pointers, length N); y is overwritten */
+int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x_dev, double* y_dev, void* stream);
+/* select kernel path: 0 = auto (fused), 1 = generic K1 composition, 2 = fused */
+int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path);
+int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* stencil_ok, double* stencil_dev);
+int mfwq_stiffness_flops(mfwq_stiffness_t h, long long* flops);
+void mfwq_stiffness_destroy(mfwq_stiffness_t h);
+
+/* ---------------- fast diagonalisation preconditioner ---------------- */
+typedef struct mfwq_fd_s* mfwq_fd_t;
+/* K3/M3: host row-major (n_l x n_l) interior 1D stiffness / mass per direction */
+int mfwq_fd_create(const int* n3, const double* const* K3, const double* const* M3, double sigma, mfwq_fd_t* out);
+int mfwq_fd_apply(mfwq_fd_t h, const double* r_dev, double* z_dev, void* stream);
+/* host copies of eigenvalues (n) and M-orthonormal eigenvectors U (row-major n x n) */
+int mfwq_fd_eigen(mfwq_fd_t h, int dir, double* lam, double* U);
+void mfwq_fd_destroy(mfwq_fd_t h);
+
+/* ---------------- preconditioned CG (device-resident) ---------------- */
+typedef struct {
+  int iterations;
+  int converged;
+  int matvecs;
+  int precond_applies;
+  int n_residuals; /* entries written to `residuals` (host, capacity maxit+1) */
+} mfwq_krylov_report;
+
+/* P may be NULL (identity).  b_dev, x_dev: device vectors of length N. */
+int mfwq_pcg_solve(mfwq_stiffness_t A, mfwq_fd_t P, const double* b_dev, double* x_dev, double tol, int maxit,
+                   double* residuals, mfwq_krylov_report* report, void* stream);
+
+/* dense Kronecker apply y (+)= (A_d x ... x A_1) x on the device, direction d
+   first (kron.py:70-100); A_l host row-major (rows[l] x cols[l]), d <= 3 */
+int mfwq_kron_apply(int d, const int* rows, const int* cols, const double* const* A_host, const double* x_dev,
+                    double* y_dev, int accumulate, void* stream);
+
+/* device dot product (test helper) */
+int mfwq_dot(const double* a_dev, const double* b_dev, long long n, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFWQ_H_ */

@@ -1,0 +1,105 @@
+"""ctypes binding of libmfwq.so (include/mfwq.h).
+
+The product path has no fallback: if the shared library is missing or no
+CUDA device is present, every operator raises instead of computing on the
+CPU.
+"""
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .errors import (DegenerateGeometryError, EigenSolveError,
+                     IndefiniteOperatorError, WQConstructionError)
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmfwq.so")
+
+_lib = None
+
+dp = C.POINTER(C.c_double)
+ip = C.POINTER(C.c_int)
+
+
+class StiffnessDesc(C.Structure):
+    _fields_ = [("p", C.c_int * 3), ("nknots", C.c_int * 3), ("knots", dp * 3),
+                ("npts", C.c_int * 3), ("pts", dp * 3),
+                ("indptr", ip * 18), ("indices", ip * 18), ("data", dp * 18)]
+
+
+class KrylovReportC(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("matvecs", C.c_int),
+                ("precond_applies", C.c_int), ("n_residuals", C.c_int)]
+
+
+_SIGS = {
+    "mfwq_last_error": (C.c_char_p, []),
+    "mfwq_version": (C.c_int, []),
+    "mfwq_rule1d_build": (C.c_int, [C.c_int, C.c_int, dp, C.POINTER(C.c_void_p)]),
+    "mfwq_rule1d_sizes": (C.c_int, [C.c_void_p, ip, ip, ip, ip]),
+    "mfwq_rule1d_export": (C.c_int, [C.c_void_p, dp, C.POINTER(ip), C.POINTER(ip), C.POINTER(dp)]),
+    "mfwq_rule1d_destroy": (None, [C.c_void_p]),
+    "mfwq_univariate_km": (C.c_int, [C.c_int, C.c_int, dp, dp, dp]),
+    "mfwq_stiffness_create": (C.c_int, [C.POINTER(StiffnessDesc), C.POINTER(C.c_void_p)]),
+    "mfwq_stiffness_set_geometry": (C.c_int, [C.c_void_p, C.c_int, dp, dp, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mfwq_stiffness_set_coeffs": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]),
+    "mfwq_stiffness_get_coeff": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "mfwq_stiffness_sizes": (C.c_int, [C.c_void_p, ip, ip, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "mfwq_stiffness_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mfwq_stiffness_set_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "mfwq_stiffness_info": (C.c_int, [C.c_void_p, ip, ip, dp]),
+    "mfwq_stiffness_flops": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
+    "mfwq_stiffness_destroy": (None, [C.c_void_p]),
+    "mfwq_fd_create": (C.c_int, [ip, C.POINTER(dp), C.POINTER(dp), C.c_double, C.POINTER(C.c_void_p)]),
+    "mfwq_fd_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mfwq_fd_eigen": (C.c_int, [C.c_void_p, C.c_int, dp, dp]),
+    "mfwq_fd_destroy": (None, [C.c_void_p]),
+    "mfwq_pcg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                 dp, C.POINTER(KrylovReportC), C.c_void_p]),
+    "mfwq_dot": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, dp, C.c_void_p]),
+    "mfwq_kron_apply": (C.c_int, [C.c_int, ip, ip, C.POINTER(dp), C.c_void_p, C.c_void_p, C.c_int,
+                                  C.c_void_p]),
+}
+
+EXPORTED = sorted(_SIGS)
+
+
+def lib():
+    """Load (once) and return the ctypes handle; raises if the .so is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} not built: run `python -m paper_1712_08565_b200.build` "
+                "(no CPU fallback exists for the MF-WQ hot path)")
+        h = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = h
+    return _lib
+
+
+_CODES = {1: ValueError, 2: WQConstructionError, 3: DegenerateGeometryError, 4: EigenSolveError,
+          5: IndefiniteOperatorError, 6: RuntimeError, 7: NotImplementedError, 8: RuntimeError}
+
+
+def check(rc):
+    if rc != 0:
+        msg = lib().mfwq_last_error().decode(errors="replace")
+        exc = _CODES.get(rc, RuntimeError)
+        if exc is WQConstructionError:
+            raise exc(-1, float("nan"), msg)
+        if exc is DegenerateGeometryError:
+            raise exc(None, float("nan"), msg)
+        raise exc(msg)
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(dp)
+
+
+def iptr(a: np.ndarray):
+    return a.ctypes.data_as(ip)

@@ -1,0 +1,217 @@
+// extern "C" boundary of libmfwq.so (declared in include/mfwq.h).
+#include <cstring>
+#include <string>
+
+#include "../../include/mfwq.h"
+#include "ops.h"
+
+using namespace mfwq;
+
+struct mfwq_rule1d_s { Rule1D r; int nfun; };
+struct mfwq_stiffness_s { Stiffness op; };
+struct mfwq_fd_s { FastDiag fd; };
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return MFWQ_OK;
+  } catch (const ValueErr& e) {
+    g_err = e.what();
+    return MFWQ_E_VALUE;
+  } catch (const WQErr& e) {
+    g_err = e.what();
+    return MFWQ_E_WQ;
+  } catch (const DegenerateErr& e) {
+    g_err = e.what();
+    return MFWQ_E_DEGENERATE;
+  } catch (const EigenErr& e) {
+    g_err = e.what();
+    return MFWQ_E_EIGEN;
+  } catch (const IndefiniteErr& e) {
+    g_err = e.what();
+    return MFWQ_E_INDEFINITE;
+  } catch (const CudaErr& e) {
+    g_err = e.what();
+    return MFWQ_E_CUDA;
+  } catch (const NotImplErr& e) {
+    g_err = e.what();
+    return MFWQ_E_NOTIMPL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MFWQ_E_INTERNAL;
+  }
+}
+
+extern "C" {
+
+const char* mfwq_last_error(void) { return g_err.c_str(); }
+int mfwq_version(void) { return 1; }
+
+int mfwq_rule1d_build(int p, int nknots, const double* knots, mfwq_rule1d_t* out) {
+  return guard([&] {
+    Knots kv(p, knots, nknots);
+    auto* h = new mfwq_rule1d_s{build_rule(kv), kv.nfun()};
+    *out = h;
+  });
+}
+
+int mfwq_rule1d_sizes(mfwq_rule1d_t r, int* npts, int* nfun, int* extra, int* nnz6) {
+  return guard([&] {
+    *npts = int(r->r.pts.size());
+    *nfun = r->nfun;
+    *extra = r->r.extra;
+    for (int k = 0; k < 4; ++k) nnz6[k] = int(r->r.W[k].data.size());
+    for (int k = 0; k < 2; ++k) nnz6[4 + k] = int(r->r.B[k].data.size());
+  });
+}
+
+int mfwq_rule1d_export(mfwq_rule1d_t r, double* pts, int* const* indptr6, int* const* indices6, double* const* data6) {
+  return guard([&] {
+    std::memcpy(pts, r->r.pts.data(), r->r.pts.size() * sizeof(double));
+    for (int k = 0; k < 6; ++k) {
+      const Csr& c = k < 4 ? r->r.W[k] : r->r.B[k - 4];
+      std::memcpy(indptr6[k], c.indptr.data(), c.indptr.size() * sizeof(int));
+      std::memcpy(indices6[k], c.indices.data(), c.indices.size() * sizeof(int));
+      std::memcpy(data6[k], c.data.data(), c.data.size() * sizeof(double));
+    }
+  });
+}
+
+void mfwq_rule1d_destroy(mfwq_rule1d_t r) { delete r; }
+
+int mfwq_univariate_km(int p, int nknots, const double* knots, double* K, double* M) {
+  return guard([&] {
+    Knots kv(p, knots, nknots);
+    std::vector<double> k, m;
+    univariate_km(kv, k, m);
+    std::memcpy(K, k.data(), k.size() * sizeof(double));
+    std::memcpy(M, m.data(), m.size() * sizeof(double));
+  });
+}
+
+int mfwq_stiffness_create(const mfwq_stiffness_desc* d, mfwq_stiffness_t* out) {
+  return guard([&] {
+    auto* h = new mfwq_stiffness_s();
+    try {
+      h->op.init(d->p, d->nknots, d->knots, d->npts, d->pts, d->indptr, d->indices, d->data);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int mfwq_stiffness_set_geometry(mfwq_stiffness_t h, int kind, const double* affine9, const double* K9,
+                                const double* J_dev, const double* Kfield_dev, void* stream) {
+  return guard([&] {
+    if (kind < 0 || kind > 3) throw ValueErr("unknown geometry kind");
+    if (kind == MFWQ_GEOM_JACOBIAN && !J_dev) throw ValueErr("JACOBIAN geometry needs J_dev");
+    h->op.set_geometry(kind, affine9, K9, J_dev, Kfield_dev, (cudaStream_t)stream);
+  });
+}
+
+int mfwq_stiffness_set_coeffs(mfwq_stiffness_t h, const double* const* grids, void* stream) {
+  return guard([&] { h->op.set_coeffs(grids, (cudaStream_t)stream); });
+}
+
+int mfwq_stiffness_get_coeff(mfwq_stiffness_t h, int key, double* out, void* stream) {
+  return guard([&] {
+    if (key < 0 || key > 5) throw ValueErr("coefficient key out of range");
+    if (!h->op.coeffs_ready) throw ValueErr("coefficient grids not set");
+    h->op.get_coeffs(key, out, (cudaStream_t)stream);
+  });
+}
+
+int mfwq_stiffness_sizes(mfwq_stiffness_t h, int* n3, int* m3, long long* N, long long* Nq) {
+  return guard([&] {
+    for (int l = 0; l < 3; ++l) {
+      n3[l] = h->op.dir[l].n;
+      m3[l] = h->op.dir[l].m;
+    }
+    *N = h->op.N;
+    *Nq = h->op.Nq;
+  });
+}
+
+int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x, double* y, void* stream) {
+  return guard([&] { h->op.apply(x, y, (cudaStream_t)stream); });
+}
+
+int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path) {
+  return guard([&] {
+    if (path < 0 || path > 2) throw ValueErr("path must be 0, 1 or 2");
+    h->op.path = path;
+  });
+}
+
+int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* stencil_ok, double* stencil_dev) {
+  return guard([&] {
+    *term_mask = h->op.term_mask();
+    *stencil_ok = h->op.stencil.ok ? 1 : 0;
+    *stencil_dev = h->op.stencil.max_dev;
+  });
+}
+
+int mfwq_stiffness_flops(mfwq_stiffness_t h, long long* flops) {
+  return guard([&] { *flops = h->op.flops; });
+}
+
+void mfwq_stiffness_destroy(mfwq_stiffness_t h) { delete h; }
+
+int mfwq_fd_create(const int* n3, const double* const* K3, const double* const* M3, double sigma, mfwq_fd_t* out) {
+  return guard([&] {
+    auto* h = new mfwq_fd_s();
+    try {
+      h->fd.init(n3, K3, M3, sigma);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int mfwq_fd_apply(mfwq_fd_t h, const double* r, double* z, void* stream) {
+  return guard([&] { h->fd.apply(r, z, (cudaStream_t)stream); });
+}
+
+int mfwq_fd_eigen(mfwq_fd_t h, int dir, double* lam, double* U) {
+  return guard([&] {
+    if (dir < 0 || dir > 2) throw ValueErr("direction out of range");
+    std::memcpy(lam, h->fd.lam_h[dir].data(), h->fd.lam_h[dir].size() * sizeof(double));
+    std::memcpy(U, h->fd.U_h[dir].data(), h->fd.U_h[dir].size() * sizeof(double));
+  });
+}
+
+void mfwq_fd_destroy(mfwq_fd_t h) { delete h; }
+
+int mfwq_pcg_solve(mfwq_stiffness_t A, mfwq_fd_t P, const double* b, double* x, double tol, int maxit,
+                   double* residuals, mfwq_krylov_report* rep, void* stream) {
+  return guard([&] {
+    std::vector<double> hist;
+    KrylovOut o;
+    pcg_solve(A->op, P ? &P->fd : nullptr, b, x, A->op.N, tol, maxit, hist, o, (cudaStream_t)stream);
+    rep->iterations = o.iterations;
+    rep->converged = o.converged;
+    rep->matvecs = o.matvecs;
+    rep->precond_applies = o.precs;
+    rep->n_residuals = int(hist.size());
+    std::memcpy(residuals, hist.data(), hist.size() * sizeof(double));
+  });
+}
+
+int mfwq_kron_apply(int d, const int* rows, const int* cols, const double* const* A, const double* x, double* y,
+                    int accumulate, void* stream) {
+  return guard([&] { kron_apply_dense(d, rows, cols, A, x, y, accumulate, (cudaStream_t)stream); });
+}
+
+int mfwq_dot(const double* a, const double* b, long long n, double* out, void* stream) {
+  return guard([&] { *out = dev_dot(a, b, n, (cudaStream_t)stream); });
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal C++ interfaces of the MF-WQ B200 library (no CUDA syntax here).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <array>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mfwq {
+
+enum GeomKind { GEOM_IDENTITY = 0, GEOM_RING = 1, GEOM_AFFINE = 2, GEOM_JACOBIAN = 3 };
+
+// Per-direction data of the tensor-product WQ discretisation.
+struct Dir1D {
+  int p = 0, n_el = 0;
+  int n = 0;  // interior DoFs
+  int m = 0;  // quadrature points
+  std::vector<double> knots, pts;
+  std::vector<int> elem_q0;  // first q of element e (size n_el+1, last = m)
+  Band B[2];                 // (m x n) interior columns of colloc[0], colloc[1]
+  Band W[4];                 // (n x m) interior rows of weights (0,0),(0,1),(1,0),(1,1)
+  DevBuf<double> pts_d;
+};
+
+// Interior-tile stencil description (uniform knots; see fused kernel).
+struct StencilInfo {
+  bool ok = false;
+  double max_dev = 0.0;
+};
+
+class Stiffness {
+ public:
+  Dir1D dir[3];
+  long long N = 0, Nq = 0;
+  int m1p = 0;                    // padded x pitch of the coefficient grids
+  DevBuf<double> coeff;           // 6 grids, (a,b) = 00,01,02,11,12,22
+  bool grid_nonzero[6] = {true, true, true, true, true, true};
+  bool coeffs_ready = false;
+  long long flops = 0;            // CostMeter count of one apply (kron.py:90-96)
+  int path = 0;                   // 0 = auto, 1 = generic (K1), 2 = fused
+  StencilInfo stencil;
+  long long nnz_[3][6] = {};      // interior-restricted nnz per direction: B0,B1,W00,W01,W10,W11
+
+  // generic-path scratch
+  DevBuf<double> g_, t_, s1_, s2_;
+  DevBuf<int> flag_;
+
+  void init(const int* p, const int* nknots, const double* const* knots, const int* npts,
+            const double* const* pts, const int* const* indptr, const int* const* indices,
+            const double* const* data);
+  // Coefficient grids C = det J J^-1 K J^-T (operators.py:64-84).
+  void set_geometry(int kind, const double* affine9, const double* K9, const double* J_dev,
+                    const double* Kfield_dev, cudaStream_t s);
+  void set_coeffs(const double* const* grids_dev, cudaStream_t s);
+  void get_coeffs(int key, double* out_dev, cudaStream_t s) const;
+  void apply(const double* x, double* y, cudaStream_t s);
+  void apply_generic(const double* x, double* y, cudaStream_t s);
+  void apply_fused(const double* x, double* y, cudaStream_t s);
+  size_t grid_elems() const { return size_t(dir[2].m) * dir[1].m * m1p; }
+  int term_mask() const;
+ private:
+  void compute_flops();
+  void detect_nonzero(cudaStream_t s);
+  void analyse_stencil();
+};
+
+class FastDiag {
+ public:
+  int n[3] = {0, 0, 0};
+  long long N = 0;
+  double sigma = 0;
+  std::vector<double> lam_h[3], U_h[3];  // U row-major n x n (U[i][k] = eigvec k, comp i)
+  DevBuf<double> U[3], Ut[3], lam[3];
+  DevBuf<double> s1_, s2_;
+  void init(const int* n, const double* const* K, const double* const* M, double sigma);
+  void apply(const double* r, double* z, cudaStream_t s);
+};
+
+struct KrylovOut {
+  int iterations = 0, converged = 0, matvecs = 0, precs = 0;
+};
+
+// device-resident PCG (solvers.py:137-173)
+void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long N, double tol, int maxit,
+               std::vector<double>& hist, KrylovOut& out, cudaStream_t s);
+
+void kron_apply_dense(int d, const int* rows, const int* cols, const double* const* A, const double* x, double* y,
+                      int accumulate, cudaStream_t s);
+
+// vector kernels
+double dev_dot(const double* a, const double* b, long long N, cudaStream_t s);
+
+}  // namespace mfwq

@@ -1,0 +1,158 @@
+"""Matrix-free WQ stiffness operator on B200 (mirrors operators.py).
+
+``setup_stiffness(space, rule, geom, K=None)`` returns an object whose
+``apply(v, meter=None)`` runs the MF-WQ matvec (Algorithm 2,
+operators.py:185-204) in hand-written sm_100a kernels through the C-ABI
+(include/mfwq.h).  ``rule`` may be this package's ``TensorRule`` or the
+reference's own (duck-typed: ``rules[l].weights[(a,b)]``,
+``rules[l].colloc[b]``, ``rules[l].points``, ``rules[l].kv``).
+"""
+
+import ctypes as C
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _dev, _lib
+from .errors import DegenerateGeometryError  # noqa: F401  (re-export)
+from .geometry import device_kind
+from .kron import CostMeter, tensor_grid
+
+#: nominal flop charge per coefficient value (operators.py:19-22)
+COEFF_EVAL_FLOPS = 60
+
+_KEYS = ((0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2))
+
+
+def _csr(A):
+    A = sp.csr_matrix(A)
+    return (np.ascontiguousarray(A.indptr, dtype=np.int32), np.ascontiguousarray(A.indices, dtype=np.int32),
+            np.ascontiguousarray(A.data, dtype=float))
+
+
+class StiffnessOperator:
+    """Matrix-free weighted-quadrature stiffness operator (interior space)."""
+
+    def __init__(self, space, rule, geom, K=None, on_the_fly=False):
+        if on_the_fly:
+            raise NotImplementedError("on-the-fly coefficient mode is not built yet (SURVEY 8(f) rank 1)")
+        _dev.require_cuda()
+        if getattr(space, "dim", 3) != 3 or len(rule.rules) != 3:
+            raise NotImplementedError("the B200 operator is three-dimensional")
+        self.space, self.rule, self.geom, self.K = space, rule, geom, K
+        self.on_the_fly = False
+        self.d = 3
+        self.n_dofs = int(np.prod(space.n_per_dir))
+        L = _lib.lib()
+        keep = []
+        desc = _lib.StiffnessDesc()
+        for l, r in enumerate(rule.rules):
+            kv = r.kv
+            knots = np.ascontiguousarray(kv.knots, dtype=float)
+            pts = np.ascontiguousarray(r.points, dtype=float)
+            keep += [knots, pts]
+            desc.p[l] = int(kv.degree)
+            desc.nknots[l] = len(knots)
+            desc.knots[l] = _lib.dptr(knots)
+            desc.npts[l] = len(pts)
+            desc.pts[l] = _lib.dptr(pts)
+            mats = [r.weights[(0, 0)], r.weights[(0, 1)], r.weights[(1, 0)], r.weights[(1, 1)],
+                    r.colloc[0], r.colloc[1]]
+            for k, M in enumerate(mats):
+                ip, ix, dv = _csr(M)
+                keep += [ip, ix, dv]
+                desc.indptr[6 * l + k] = _lib.iptr(ip)
+                desc.indices[6 * l + k] = _lib.iptr(ix)
+                desc.data[6 * l + k] = _lib.dptr(dv)
+        h = C.c_void_p()
+        _lib.check(L.mfwq_stiffness_create(C.byref(desc), C.byref(h)))
+        self._h = h
+        n3 = np.zeros(3, np.int32)
+        m3 = np.zeros(3, np.int32)
+        N, Nq = C.c_longlong(), C.c_longlong()
+        _lib.check(L.mfwq_stiffness_sizes(h, _lib.iptr(n3), _lib.iptr(m3), C.byref(N), C.byref(Nq)))
+        self.n, self.m, self.n_points = tuple(int(v) for v in n3), tuple(int(v) for v in m3), Nq.value
+        if N.value != self.n_dofs:
+            raise ValueError("rule and space disagree on the number of DoFs")
+        self._set_geometry(geom, K)
+        fl = C.c_longlong()
+        _lib.check(L.mfwq_stiffness_flops(h, C.byref(fl)))
+        self.apply_flops = fl.value
+        self.setup_flops = COEFF_EVAL_FLOPS * self.n_points * 6
+
+    # -- coefficient grids (operators.py:64-84) --------------------------------
+    def _points(self):
+        return np.stack(tensor_grid([r.points for r in self.rule.rules]), axis=1)
+
+    def _set_geometry(self, geom, K):
+        L = _lib.lib()
+        s = C.c_void_p(_dev.stream_ptr())
+        kind, A = device_kind(geom)
+        K9 = None
+        Kfield = None
+        if K is not None:
+            if callable(K):
+                xi = self._points()
+                Kfield = _dev.to_device(np.asarray(K(geom.evaluate(xi)), dtype=float).reshape(-1))[0]
+            else:
+                Ka = np.asarray(K, dtype=float)
+                if Ka.shape == (3, 3):
+                    K9 = np.ascontiguousarray(Ka)
+                else:
+                    Kfield = _dev.to_device(Ka.reshape(-1))[0]
+        J = None
+        if kind == 3:
+            xi = self._points()
+            J = _dev.to_device(np.asarray(geom.jacobian(xi), dtype=float).reshape(-1))[0]
+        rc = L.mfwq_stiffness_set_geometry(
+            self._h, kind, _lib.dptr(A) if A is not None else None, _lib.dptr(K9) if K9 is not None else None,
+            C.c_void_p(J.data_ptr()) if J is not None else None,
+            C.c_void_p(Kfield.data_ptr()) if Kfield is not None else None, s)
+        _lib.check(rc)
+
+    @property
+    def coeff_scalars(self) -> int:
+        return 6 * self.n_points
+
+    @property
+    def coeffs(self):
+        """The six symmetric grids keyed (a<=b) as host arrays (operators.py:84)."""
+        out = {}
+        for k, key in enumerate(_KEYS):
+            g = _dev.empty(self.n_points)
+            _lib.check(_lib.lib().mfwq_stiffness_get_coeff(self._h, k, C.c_void_p(g.data_ptr()),
+                                                           C.c_void_p(_dev.stream_ptr())))
+            out[key] = g.cpu().numpy()
+        return out
+
+    def set_path(self, path: str):
+        """'auto' | 'generic' | 'fused' kernel path (all on the GPU)."""
+        _lib.check(_lib.lib().mfwq_stiffness_set_path(self._h, {"auto": 0, "generic": 1, "fused": 2}[path]))
+
+    def info(self):
+        tm, so, dev = C.c_int(), C.c_int(), C.c_double()
+        _lib.check(_lib.lib().mfwq_stiffness_info(self._h, C.byref(tm), C.byref(so), C.byref(dev)))
+        return {"term_mask": tm.value, "stencil_ok": bool(so.value), "stencil_dev": dev.value}
+
+    # -- apply (operators.py:185-204) -----------------------------------------
+    def apply(self, v, meter: CostMeter | None = None, out=None):
+        x, host = _dev.to_device(v, self.n_dofs)
+        y = out if out is not None else _dev.empty(self.n_dofs)
+        _lib.check(_lib.lib().mfwq_stiffness_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                                   C.c_void_p(_dev.stream_ptr())))
+        if meter is not None:
+            meter.add_flops(self.apply_flops)
+        return _dev.back(y, host)
+
+    __call__ = apply
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.mfwq_stiffness_destroy(h)
+            self._h = None
+
+
+def setup_stiffness(space, rule, geom, K=None, on_the_fly=False) -> StiffnessOperator:
+    """operators.py:227-228."""
+    return StiffnessOperator(space, rule, geom, K=K, on_the_fly=on_the_fly)

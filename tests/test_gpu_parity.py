@@ -1,0 +1,158 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+outputs and the CPU oracle.  Bar (BASELINE north_star): matvec rel. error
+<= 1e-12, PCG iterations within +-1, solution rel. difference <= 1e-9."""
+import numpy as np
+import pytest
+
+import paper_1712_08565_b200 as M
+from oracle import mfwq_oracle as O
+
+from gpu_helpers import SHEAR, geom_of, golden_rule, relerr
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-12
+
+
+@pytest.mark.parametrize("path", ["generic", "fused"])
+def test_matvec_matches_reference(golden, path):
+    name, g = golden
+    rule, space = golden_rule(g)
+    A = M.setup_stiffness(space, rule, geom_of(g["geom"]))
+    A.set_path(path)
+    x = np.random.default_rng(0).standard_normal(space.n_dofs)
+    meter = M.CostMeter()
+    y = A.apply(x, meter)
+    assert relerr(y, g["y"]) <= MATVEC_TOL, (name, relerr(y, g["y"]))
+    assert meter.flops == int(g["flops"])
+
+
+def test_fd_apply_matches_reference(golden):
+    name, g = golden
+    if "fd_y" not in g:
+        pytest.skip("no FD output stored")
+    rule, space = golden_rule(g)
+    P = M.FDPreconditioner(space)
+    x = np.random.default_rng(0).standard_normal(space.n_dofs)
+    z = P.apply(x)
+    tol = 1e-11 if int(g["p"]) <= 6 else 1e-8  # M-conditioning grows ~1e8 at p=8 (test_acceptance.py:115-135)
+    assert relerr(z, g["fd_y"]) <= tol, (name, relerr(z, g["fd_y"]))
+    assert np.abs(np.sort(P.lams[0]) - g["lam"]).max() <= 1e-9 * np.abs(g["lam"]).max()
+
+
+def test_pcg_matches_reference(golden):
+    name, g = golden
+    if "u" not in g:
+        pytest.skip("no PCG output stored")
+    rule, space = golden_rule(g)
+    A = M.setup_stiffness(space, rule, geom_of(g["geom"]))
+    P = M.FDPreconditioner(space)
+    u, rep = M.cg(A.apply, g["b"], P.apply, tol=1e-8)
+    assert rep.converged
+    assert abs(rep.iterations - int(g["iters"])) <= 1, (name, rep.iterations, int(g["iters"]))
+    assert relerr(u, g["u"]) <= 1e-9, (name, relerr(u, g["u"]))
+    assert rep.residuals[0] == 1.0 and len(rep.residuals) == rep.iterations + 1
+    assert rep.matvecs == rep.iterations and rep.precond_applies == rep.iterations
+
+
+@pytest.mark.parametrize("kind", ["identity", "ring", "shear"])
+def test_coefficient_grids_match_oracle(kind):
+    p, n_el = 3, 5
+    space = M.tensor_space(p, n_el)
+    rule = M.build_tensor_rule(space)
+    A = M.setup_stiffness(space, rule, geom_of(kind))
+    orules = [O.rule_1d(O.uniform_knots(p, n_el))] * 3
+    ref = O.stiffness_coeffs(orules, O.jac_for(kind, SHEAR))
+    got = A.coeffs
+    for key, r in ref.items():
+        assert np.abs(got[key] - r).max() <= 1e-14 * max(1.0, np.abs(r).max()), (kind, key)
+    if kind == "identity":
+        for key in ((0, 1), (0, 2), (1, 2)):
+            assert not got[key].any()
+    assert A.coeff_scalars == 6 * rule.n_points
+
+
+def test_degenerate_geometry_raises():
+    folded = M.GeometryMap(3, "folded", lambda xi: xi,
+                           lambda xi: np.broadcast_to(np.diag([1.0, -1.0, 1.0]), (len(xi), 3, 3)).copy())
+    space = M.tensor_space(1, 2)
+    with pytest.raises(M.DegenerateGeometryError):
+        M.setup_stiffness(space, M.build_tensor_rule(space), folded)
+
+
+def test_zero_vector_and_length_mismatch():
+    space = M.tensor_space(2, 3)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map())
+    assert np.array_equal(A.apply(np.zeros(space.n_dofs)), np.zeros(space.n_dofs))
+    with pytest.raises(ValueError):
+        A.apply(np.zeros(space.n_dofs + 1))
+    P = M.FDPreconditioner(space)
+    assert np.array_equal(P.apply(np.zeros(space.n_dofs)), np.zeros(space.n_dofs))
+    with pytest.raises(ValueError):
+        P.apply(np.zeros(space.n_dofs + 1))
+    with pytest.raises(ValueError):
+        M.FDPreconditioner(space, sigma=-1.0)
+
+
+@pytest.mark.parametrize("p,n_el", [(2, 8), (5, 8), (7, 8), (3, 16)])
+def test_fd_self_inverse(p, n_el):
+    """solvers test_self_inverse (test_solvers.py:35-45) on the device."""
+    space = M.tensor_space(p, n_el)
+    P = M.FDPreconditioner(space)
+    v = np.random.default_rng(0).standard_normal(space.n_dofs)
+    back = P.apply(P.apply_forward(v))
+    assert relerr(back, v) <= 1e-10
+
+
+def test_native_rule_end_to_end_cfg1():
+    """Package-built rule (C++ WQ) + GPU operator vs the reference golden at cfg 1."""
+    from conftest import load_golden
+    g = load_golden("cfg1_cube_p3_n16")
+    space = M.tensor_space(3, 16)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.identity_map(3))
+    x = np.random.default_rng(0).standard_normal(space.n_dofs)
+    assert relerr(A.apply(x), g["y"]) <= MATVEC_TOL
+    P = M.FDPreconditioner(space)
+    u, rep = M.cg(A.apply, g["b"], P.apply, tol=1e-8)
+    assert rep.iterations == int(g["iters"]) == 1
+    assert relerr(u, g["u"]) <= 1e-9
+
+
+def test_cg_generic_callables():
+    b = np.random.default_rng(0).standard_normal(50)
+    x, rep = M.cg(lambda v: v, b, tol=1e-12)
+    assert rep.iterations == 1 and np.allclose(x, b)
+    x, rep = M.cg(lambda v: v, np.zeros(10))
+    assert rep.iterations == 0 and not x.any()
+    with pytest.raises(M.IndefiniteOperatorError):
+        M.cg(lambda v: -v, np.ones(5))
+
+
+def test_cg_device_indefinite_and_maxit():
+    space = M.tensor_space(2, 4)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map())
+    b = np.random.default_rng(3).standard_normal(space.n_dofs)
+    x, rep = M.cg(A.apply, b, tol=1e-14, maxit=3)
+    assert not rep.converged and rep.iterations == 3 and len(rep.residuals) == 4
+    x, rep = M.cg(A.apply, np.zeros(space.n_dofs))
+    assert rep.iterations == 0 and rep.residuals == [0.0]
+
+
+def test_kron_apply_vs_oracle():
+    rng = np.random.default_rng(7)
+    fs = [rng.standard_normal((3, 4)), rng.standard_normal((5, 2)), rng.standard_normal((2, 3))]
+    x = rng.standard_normal(4 * 2 * 3)
+    assert relerr(M.kron_apply(fs, x), O.kron_apply(fs, x)) <= 1e-13
+    meter = M.CostMeter()
+    M.kron_apply([np.ones((4, 4))] * 3, np.ones(64), meter)
+    assert meter.flops == 2 * 4 * 4 * (16 + 16 + 16)
+
+
+def test_torch_device_inputs_stay_on_device():
+    import torch
+    space = M.tensor_space(3, 6)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map())
+    x = torch.randn(space.n_dofs, dtype=torch.float64, device="cuda")
+    y = A.apply(x)
+    assert isinstance(y, torch.Tensor) and y.is_cuda
+    assert relerr(y.cpu().numpy(), A.apply(x.cpu().numpy())) == 0.0
