@@ -1,0 +1,374 @@
+"""MF-WQ B200 benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], "cfg2"): unit-cube Poisson, identity
+geometry, n_el = 128 per direction, maximal-regularity splines p = 2..6,
+fp64.  One step = one MF-WQ stiffness matvec at every degree of the sweep on
+x ~ N(0,1) (seed 0).  value = DoFs processed / second over the whole sweep.
+The coefficient grids (0.4-0.9 GB per degree) exceed the 126 MB L2, so no
+explicit flush is needed between iterations.
+
+Extra keys: per-degree times, roofline of the matvec kernel (HBM bound per
+BASELINE; fp64 fraction alongside), e2e through the public API with pinned
+host buffers, the CPU baseline (oracle port on the host cores), and an
+optional cfg-3 FD-PCG time-to-solution (--pcg).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--pcg 0|1]
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SWEEP = (2, 3, 4, 5, 6)
+N_EL = 128
+METRIC = "MF-WQ fp64 matvec DoF/s (cfg2 sweep p=2-6, n_el=128)"
+UNIT = "DoF/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pcg", type=int, default=1)
+    ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--path", default="auto", choices=["auto", "generic", "fused"])
+    return ap.parse_args()
+
+
+def dist_info():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------------------- clocks
+REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
+           "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        for ln in self.lines:
+            try:
+                a, b, c = [x.strip() for x in ln.split(",")]
+                sm.append(float(a))
+                mx = max(mx, float(b))
+                bits = int(c, 16)
+                for i, name in enumerate(REASONS):
+                    if bits & (1 << i) and name != "gpu_idle":
+                        reasons.add(name)
+            except ValueError:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- peaks
+def peaks():
+    out = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)", "fp64_tflops": 37.1,
+           "fp64_src": "DMMA probe tools/fp64_peak (profiles/fp64_peak_r01.json)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            m = json.load(fh)
+        out["hbm_gbs"] = float(m["hbm_gbs"])
+        out["hbm_src"] = "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as fh:
+            f = json.load(fh)
+        out["fp64_tflops"] = max(float(f["dmma_tflops"]), float(f["dfma_tflops"]))
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
+
+
+def traffic_from_profile():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_sample(steps=None, threads=None):
+    """Oracle port (oracle/mfwq_oracle.py) on the host: one matvec per degree.
+
+    Coefficient grids for identity geometry are the exact constants the
+    reference computes there (C = I; operators.py:64-84 gives det = 1 and
+    J^-1 = I exactly), built directly so the sample times the matvec only.
+    """
+    from oracle import mfwq_oracle as O
+
+    degs = SWEEP if steps is None else [SWEEP[i % len(SWEEP)] for i in range(steps)]
+    built = {}
+    total_n, total_t = 0, 0.0
+    per = {}
+    for p in degs:
+        if p not in built:
+            kv = O.uniform_knots(p, N_EL)
+            rule = O.rule_1d(kv)
+            nq = len(rule.pts) ** 3
+            C = {k: (np.ones(nq) if k[0] == k[1] else np.zeros(nq)) for k in O.COEFF_KEYS}
+            built[p] = O.Stiffness([rule] * 3, C)
+        A = built[p]
+        x = np.random.default_rng(0).standard_normal(A.N)
+        t0 = time.perf_counter()
+        A.apply(x)
+        dt = time.perf_counter() - t0
+        total_n += A.N
+        total_t += dt
+        per.setdefault(p, []).append(dt)
+    return total_n / total_t, per, total_t
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    cpu_sample(steps=args.warmup)  # warm-up (also builds the rules)
+    val, per, tot = cpu_sample(steps=args.steps)
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "cfg2 unit-cube MF-WQ matvec, n_el=128, p=2..6 sweep (one degree per step)",
+                       "sweep": list(SWEEP), "n_el": N_EL, "geometry": "identity", "parallelism": "host"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} oracle matvecs cycling p=2..6 at n_el=128 (scipy CSR "
+                                       "sum-factorisation, single-threaded like the reference)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "per_degree_s": {str(k): statistics.median(v) for k, v in per.items()}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1712_08565_b200 as M
+    from paper_1712_08565_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ops = {}
+    for p in SWEEP:
+        space = M.tensor_space(p, N_EL)
+        rule = M.build_tensor_rule(space)
+        A = M.setup_stiffness(space, rule, M.identity_map(3))
+        if args.path != "auto":
+            A.set_path(args.path)
+        x = torch.from_numpy(np.random.default_rng(0).standard_normal(space.n_dofs)).to(dev)
+        y = torch.empty_like(x)
+        info = A.info()
+        ngrids = len({(min(a, b), max(a, b)) for a in range(3) for b in range(3)
+                      if info["term_mask"] >> (3 * a + b) & 1})
+        ops[p] = dict(A=A, x=x, y=y, N=space.n_dofs, Nq=A.n_points, grids=ngrids,
+                      bytes=8 * (2 * space.n_dofs + ngrids * A.n_points), flops=A.apply_flops,
+                      flops_active=A.apply_flops_active)
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        for p in SWEEP:
+            o = ops[p]
+            if evs is not None:
+                evs[p][0].record(stream)
+            o["A"].apply(o["x"], out=o["y"])
+            if evs is not None:
+                evs[p][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = _lib.lib().mfwq_launch_count()
+    per_p = {p: [] for p in SWEEP}
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        all_evs = []
+        for _ in range(args.steps):
+            evs = {p: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for p in SWEEP}
+            step(evs)
+            all_evs.append(evs)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = _lib.lib().mfwq_launch_count() - launches0
+    ms = t0.elapsed_time(t1)
+    for evs in all_evs:
+        for p in SWEEP:
+            per_p[p].append(evs[p][0].elapsed_time(evs[p][1]))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t)
+    dofs_step = sum(ops[p]["N"] for p in SWEEP)
+    value = dofs_step * args.steps * world / (ms * 1e-3)
+
+    # e2e through the public API: pinned host x -> device -> matvec -> pinned host y
+    hx = {p: torch.from_numpy(ops[p]["x"].cpu().numpy()).pin_memory() for p in SWEEP}
+    for p in SWEEP:
+        ops[p]["A"].apply(hx[p])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        for p in SWEEP:
+            ops[p]["A"].apply(hx[p])  # H2D, kernel, D2H (synchronous result on the host)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = dofs_step * e2e_steps * world / (float(e2e_t) * 1e-3)
+
+    # roofline of the matvec kernel, aggregated over the sweep
+    pk = peaks()
+    med = {p: statistics.median(per_p[p]) for p in SWEEP}
+    tot_ms = sum(med.values())
+    bytes_tot = sum(ops[p]["bytes"] for p in SWEEP)
+    flops_act = sum(ops[p]["flops_active"] for p in SWEEP)
+    achieved = bytes_tot / (tot_ms * 1e-3) / 1e9
+    fp64 = flops_act / (tot_ms * 1e-3) / 1e12
+    trf = traffic_from_profile()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "peak_src": pk["hbm_src"],
+            "traffic": trf.get("bytes_per_launch") if trf else None,
+            "traffic_src": trf.get("source") if trf else None,
+            "fp64_achieved_tflops": fp64, "fp64_peak_tflops": pk["fp64_tflops"],
+            "fp64_frac": fp64 / pk["fp64_tflops"], "fp64_src": pk["fp64_src"],
+            "algorithmic_bytes": "8*(2N + G*Nq) per matvec, G = non-zero coefficient grids (3 on identity)"}
+
+    pcg = None
+    if args.pcg and world == 1:
+        pcg = run_pcg(M, torch, dev)
+
+    if rank == 0:
+        cpu = None
+        if args.cpu_baseline and world == 1:
+            v, per, tot = cpu_sample()
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": "one oracle matvec per degree p=2..6 at n_el=128 (identical workload to one step; "
+                             f"{tot:.1f} s of single-threaded scipy CSR sum-factorisation)",
+                   "per_degree_s": {str(k): v2[0] for k, v2 in per.items()}}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "cfg2 unit-cube MF-WQ matvec, n_el=128, p=2..6 sweep per step",
+                           "sweep": list(SWEEP), "n_el": N_EL, "geometry": "identity",
+                           "x": "N(0,1) seed 0", "l2": "coefficient grids 0.4-0.9 GB per degree > 126 MB L2 (no flush)",
+                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                           "path": args.path},
+                "per_degree_us": {str(p): 1e3 * med[p] for p in SWEEP},
+                "per_degree_dofs": {str(p): ops[p]["N"] for p in SWEEP},
+                "roofline": roof,
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": UNIT,
+                        "h2d_bytes_per_step": 8 * dofs_step, "d2h_bytes_per_step": 8 * dofs_step},
+                "gpu_launches": int(launches),
+                "clocks": clk.summary(),
+                "pcg": pcg}
+        print(json.dumps(line), flush=True)
+
+
+def run_pcg(M, torch, dev):
+    """cfg 3: quarter ring, p=4, n_el=256 (17.2 M DoFs), FD-PCG to 1e-8 on b ~ N(0,1) seed 1."""
+    p, n_el = 4, 256
+    t0 = time.perf_counter()
+    space = M.tensor_space(p, n_el)
+    rule = M.build_tensor_rule(space)
+    t1 = time.perf_counter()
+    A = M.setup_stiffness(space, rule, M.quarter_ring_map())
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    P = M.FDPreconditioner(space)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    b = torch.from_numpy(np.random.default_rng(1).standard_normal(space.n_dofs)).to(dev)
+    M.cg(A.apply, b, P.apply, tol=1e-8, maxit=2)  # warm-up
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    u, rep = M.cg(A.apply, b, P.apply, tol=1e-8)
+    e1.record()
+    torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) * 1e-3
+    return {"config": "cfg3 quarter ring p=4 n_el=256", "N": space.n_dofs, "iterations": rep.iterations,
+            "converged": rep.converged, "final_rel_residual": rep.residuals[-1], "solve_s": secs,
+            "dof_iters_per_s": space.n_dofs * rep.iterations / secs,
+            "setup_s": {"wq_rule": t1 - t0, "coeff_grids": t2 - t1, "fd": t3 - t2},
+            "u_norm": float(torch.linalg.vector_norm(u))}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_info()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

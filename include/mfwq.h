@@ -46,6 +46,8 @@ extern "C" {
 
 const char* mfwq_last_error(void);
 int mfwq_version(void);
+/* number of kernels this library has launched so far (process-wide) */
+long long mfwq_launch_count(void);
 
 /* ---------------- 1D weighted-quadrature rule (host) ---------------- */
 typedef struct mfwq_rule1d_s* mfwq_rule1d_t;
@@ -92,6 +94,8 @@ int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x_dev, double* y_dev,
 int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path);
 int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* stencil_ok, double* stencil_dev);
 int mfwq_stiffness_flops(mfwq_stiffness_t h, long long* flops);
+/* same count restricted to the terms with a non-zero coefficient grid (what the kernels execute) */
+int mfwq_stiffness_flops_active(mfwq_stiffness_t h, long long* flops);
 void mfwq_stiffness_destroy(mfwq_stiffness_t h);
 
 /* ---------------- fast diagonalisation preconditioner ---------------- */

@@ -31,6 +31,9 @@ def to_device(v, n=None):
             t = t.to(torch.float64)
         t = t.contiguous()
         host = False
+    elif torch is not None and isinstance(v, torch.Tensor):  # host torch tensor (pinned -> async H2D)
+        t = v.reshape(-1).to(dtype=torch.float64).to("cuda", non_blocking=v.is_pinned())
+        host = "torch"
     else:
         a = np.ascontiguousarray(np.asarray(v, dtype=float).ravel())
         t = torch.from_numpy(a).to("cuda", non_blocking=False)
@@ -51,4 +54,9 @@ def zeros(n):
 
 
 def back(t, host):
+    if host == "torch":
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
     return t.cpu().numpy() if host else t

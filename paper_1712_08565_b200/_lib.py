@@ -36,6 +36,7 @@ class KrylovReportC(C.Structure):
 _SIGS = {
     "mfwq_last_error": (C.c_char_p, []),
     "mfwq_version": (C.c_int, []),
+    "mfwq_launch_count": (C.c_longlong, []),
     "mfwq_rule1d_build": (C.c_int, [C.c_int, C.c_int, dp, C.POINTER(C.c_void_p)]),
     "mfwq_rule1d_sizes": (C.c_int, [C.c_void_p, ip, ip, ip, ip]),
     "mfwq_rule1d_export": (C.c_int, [C.c_void_p, dp, C.POINTER(ip), C.POINTER(ip), C.POINTER(dp)]),
@@ -50,6 +51,7 @@ _SIGS = {
     "mfwq_stiffness_set_path": (C.c_int, [C.c_void_p, C.c_int]),
     "mfwq_stiffness_info": (C.c_int, [C.c_void_p, ip, ip, dp]),
     "mfwq_stiffness_flops": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
+    "mfwq_stiffness_flops_active": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "mfwq_stiffness_destroy": (None, [C.c_void_p]),
     "mfwq_fd_create": (C.c_int, [ip, C.POINTER(dp), C.POINTER(dp), C.c_double, C.POINTER(C.c_void_p)]),
     "mfwq_fd_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

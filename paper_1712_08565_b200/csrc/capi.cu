@@ -12,6 +12,7 @@ struct mfwq_stiffness_s { Stiffness op; };
 struct mfwq_fd_s { FastDiag fd; };
 
 static thread_local std::string g_err;
+long long mfwq::g_launches = 0;
 
 template <class F>
 static int guard(F&& f) {
@@ -50,6 +51,7 @@ extern "C" {
 
 const char* mfwq_last_error(void) { return g_err.c_str(); }
 int mfwq_version(void) { return 1; }
+long long mfwq_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 int mfwq_rule1d_build(int p, int nknots, const double* knots, mfwq_rule1d_t* out) {
   return guard([&] {
@@ -159,6 +161,10 @@ int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* stencil_ok, dou
 
 int mfwq_stiffness_flops(mfwq_stiffness_t h, long long* flops) {
   return guard([&] { *flops = h->op.flops; });
+}
+
+int mfwq_stiffness_flops_active(mfwq_stiffness_t h, long long* flops) {
+  return guard([&] { *flops = h->op.flops_for(h->op.term_mask()); });
 }
 
 void mfwq_stiffness_destroy(mfwq_stiffness_t h) { delete h; }

@@ -76,3 +76,9 @@ BandHost csr_to_band(const Csr& A, int r0, int r1, int c0, int c1);
 inline int ceil_div(long long a, long long b) { return int((a + b - 1) / b); }
 
 }  // namespace mfwq
+
+namespace mfwq {
+// Count of this library's kernel launches (reported by bench.py as gpu_launches).
+extern long long g_launches;
+inline void note_launch() { __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED); }
+}  // namespace mfwq

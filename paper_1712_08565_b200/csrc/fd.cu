@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(const double* __restrict
 void dgemm(const double* A, const double* B, double* C, int M, int N, int K, int lda, int ldb, int ldc, int batch,
            long long sa, long long sb, long long sc, Epi epi, cudaStream_t s) {
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
-  dgemm_kernel<<<grid, THREADS, 0, s>>>(A, B, C, M, N, K, lda, ldb, ldc, sa, sb, sc, epi);
+  dgemm_kernel<<<grid, THREADS, 0, s>>>(A, B, C, M, N, K, lda, ldb, ldc, sa, sb, sc, epi); note_launch();
   MFWQ_CUDA(cudaGetLastError());
 }
 }  // namespace gemm

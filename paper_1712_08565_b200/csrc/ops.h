@@ -60,6 +60,7 @@ class Stiffness {
   void apply_fused(const double* x, double* y, cudaStream_t s);
   size_t grid_elems() const { return size_t(dir[2].m) * dir[1].m * m1p; }
   int term_mask() const;
+  long long flops_for(int mask) const;
  private:
   void compute_flops();
   void detect_nonzero(cudaStream_t s);

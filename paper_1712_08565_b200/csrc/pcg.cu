@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(RB) update_p(double* __restrict__ p, const dou
 __global__ void copy_scalar(const double* src, double* dst) { *dst = *src; }
 
 static void dot_to(const double* a, const double* b, long long N, double* partial, double* out, cudaStream_t s) {
-  dot_partial<<<RGRID, RB, 0, s>>>(a, b, N, partial);
-  finish_sum<<<1, RB, 0, s>>>(partial, RGRID, out);
+  dot_partial<<<RGRID, RB, 0, s>>>(a, b, N, partial); note_launch();
+  finish_sum<<<1, RB, 0, s>>>(partial, RGRID, out); note_launch();
 }
 
 double dev_dot(const double* a, const double* b, long long N, cudaStream_t s) {
@@ -113,8 +113,8 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
     A.apply(p.ptr, Ap.ptr, s);
     out.matvecs++;
     dot_to(p.ptr, Ap.ptr, N, part.ptr, pAp, s);
-    update_xr<<<RGRID, RB, 0, s>>>(x, r.ptr, p.ptr, Ap.ptr, N, rz, pAp, part.ptr);
-    finish_sum<<<1, RB, 0, s>>>(part.ptr, RGRID, rr);
+    update_xr<<<RGRID, RB, 0, s>>>(x, r.ptr, p.ptr, Ap.ptr, N, rz, pAp, part.ptr); note_launch();
+    finish_sum<<<1, RB, 0, s>>>(part.ptr, RGRID, rr); note_launch();
     MFWQ_CUDA(cudaGetLastError());
     MFWQ_CUDA(cudaMemcpyAsync(h2, pAp, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     MFWQ_CUDA(cudaStreamSynchronize(s));
@@ -134,8 +134,8 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
     else MFWQ_CUDA(cudaMemcpyAsync(z.ptr, r.ptr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     out.precs++;
     dot_to(r.ptr, z.ptr, N, part.ptr, rzn, s);
-    update_p<<<RGRID, RB, 0, s>>>(p.ptr, z.ptr, N, rzn, rz);
-    copy_scalar<<<1, 1, 0, s>>>(rzn, rz);
+    update_p<<<RGRID, RB, 0, s>>>(p.ptr, z.ptr, N, rzn, rz); note_launch();
+    copy_scalar<<<1, 1, 0, s>>>(rzn, rz); note_launch();
     MFWQ_CUDA(cudaGetLastError());
   }
   out.iterations = maxit;

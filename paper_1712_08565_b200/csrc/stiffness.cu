@@ -106,26 +106,32 @@ void Stiffness::init(const int* p, const int* nknots, const double* const* knots
   analyse_stencil();
 }
 
-void Stiffness::compute_flops() {
+// CostMeter count (kron.py:90-96, operators.py:191-203) restricted to the
+// terms in `mask` (bit 3a+b); mask 0x1FF is the reference's full count.
+long long Stiffness::flops_for(int mask) const {
   const long long n1 = dir[0].n, n2 = dir[1].n, n3 = dir[2].n;
   const long long m1 = dir[0].m, m2 = dir[1].m, m3 = dir[2].m;
   // S(A; s, t) with contraction order 3, 2, 1 (kron.py:83-96)
   auto S = [&](long long z1, long long z2, long long z3, long long s1, long long s2, long long s3, long long t1,
-               long long t2) { return 2 * z3 * t1 * t2 + 2 * z2 * s3 * t1 + 2 * z1 * s3 * s2; };
+               long long t2) { (void)s1; return 2 * z3 * t1 * t2 + 2 * z2 * s3 * t1 + 2 * z1 * s3 * s2; };
   long long F = 0;
   for (int b = 0; b < 3; ++b) {
+    if (!(mask & (0x49 << b))) continue;  // no active term (a, b)
     long long z[3];
     for (int l = 0; l < 3; ++l) z[l] = nnz_[l][l == b ? 1 : 0];
     F += S(z[0], z[1], z[2], m1, m2, m3, n1, n2);
   }
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) {
+      if (!(mask & (1 << (3 * a + b)))) continue;
       long long z[3];
       for (int l = 0; l < 3; ++l) z[l] = nnz_[l][2 + 2 * (l == a) + (l == b)];
       F += S(z[0], z[1], z[2], n1, n2, n3, m1, m2) + Nq + 2 * N;
     }
-  flops = F;
+  return F;
 }
+
+void Stiffness::compute_flops() { flops = flops_for(0x1FF); }
 
 // ---------------------------------------------------------------------------
 // K5: coefficient grids (operators.py:64-84, geometry.py:47-96)
@@ -238,10 +244,10 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
   coeff_kernel<<<blocks, 256, 0, s>>>(kind, dir[0].pts_d.ptr, dir[1].pts_d.ptr, dir[2].pts_d.ptr, m1, m2, m3, m1p,
                                       a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], K9 ? 1 : 0, k[0], k[1],
                                       k[2], k[3], k[4], k[5], k[6], k[7], k[8], J_dev, Kfield_dev, coeff.ptr, G,
-                                      bad.ptr);
+                                      bad.ptr); note_launch();
   MFWQ_CUDA(cudaGetLastError());
   if (m1p > m1) {
-    pad_zero_kernel<<<148, 256, 0, s>>>(coeff.ptr, m1, m1p, (long long)m2 * m3, G);
+    pad_zero_kernel<<<148, 256, 0, s>>>(coeff.ptr, m1, m1p, (long long)m2 * m3, G); note_launch();
     MFWQ_CUDA(cudaGetLastError());
   }
   unsigned long long hbad = 0;
@@ -287,7 +293,7 @@ void Stiffness::detect_nonzero(cudaStream_t s) {
   flag_.alloc(6);
   MFWQ_CUDA(cudaMemsetAsync(flag_.ptr, 0, 6 * sizeof(int), s));
   for (int g = 0; g < 6; ++g) {
-    any_nonzero_kernel<<<148 * 4, 256, 0, s>>>(coeff.ptr + g * G, G, flag_.ptr + g);
+    any_nonzero_kernel<<<148 * 4, 256, 0, s>>>(coeff.ptr + g * G, G, flag_.ptr + g); note_launch();
     MFWQ_CUDA(cudaGetLastError());
   }
   int h[6];
@@ -351,7 +357,7 @@ static void contract(const double* in, double* out, int d1, int d2, int d3, int 
                      cudaStream_t s) {
   long long o = (long long)(ax == 0 ? A.h.rows : d1) * (ax == 1 ? A.h.rows : d2) * (ax == 2 ? A.h.rows : d3);
   int blocks = (int)std::min<long long>((o + 255) / 256, 148LL * 32);
-  band_contract_kernel<<<std::max(blocks, 1), 256, 0, s>>>(in, out, d1, d2, d3, ax, A.view(), acc);
+  band_contract_kernel<<<std::max(blocks, 1), 256, 0, s>>>(in, out, d1, d2, d3, ax, A.view(), acc); note_launch();
   MFWQ_CUDA(cudaGetLastError());
 }
 
@@ -378,7 +384,7 @@ void Stiffness::apply_generic(const double* x, double* y, cudaStream_t s) {
       int key = gkey(a, b);
       if (!grid_nonzero[key]) continue;
       int blocks = (int)std::min<long long>((Nq + 255) / 256, 148LL * 32);
-      scale_kernel<<<blocks, 256, 0, s>>>(coeff.ptr + key * G, g_.ptr, t_.ptr, m1, m1p, Nq);
+      scale_kernel<<<blocks, 256, 0, s>>>(coeff.ptr + key * G, g_.ptr, t_.ptr, m1, m1p, Nq); note_launch();
       MFWQ_CUDA(cudaGetLastError());
       auto widx = [&](int l) { return 2 * (l == a) + (l == b); };
       contract(t_.ptr, s1_.ptr, m1, m2, m3, 2, dir[2].W[widx(2)], 0, s);

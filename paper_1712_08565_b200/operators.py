@@ -78,6 +78,8 @@ class StiffnessOperator:
         fl = C.c_longlong()
         _lib.check(L.mfwq_stiffness_flops(h, C.byref(fl)))
         self.apply_flops = fl.value
+        _lib.check(L.mfwq_stiffness_flops_active(h, C.byref(fl)))
+        self.apply_flops_active = fl.value  # terms with a non-zero grid (what runs)
         self.setup_flops = COEFF_EVAL_FLOPS * self.n_points * 6
 
     # -- coefficient grids (operators.py:64-84) --------------------------------
