@@ -38,7 +38,7 @@ UNIT = "DoF/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pcg", type=int, default=1)
@@ -52,52 +52,58 @@ def dist_info():
 
 
 # ----------------------------------------------------------------------------- clocks
-REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
-           "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
+# NVML clocks-event-reason bits (nvml.h nvmlClocksEventReason*)
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
 class ClockSampler:
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    """Polls NVML (SM clock, clocks-event reasons) every ~2 ms while the timed region runs."""
+
+    def __init__(self, index, period=0.002):
+        self.index, self.period = index, period
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, rs))
+                    except pynvml.NVMLError:
+                        pass
+                    time.sleep(self.period)
+
+            self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # NVML unavailable: report no samples
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
-        for ln in self.lines:
-            try:
-                a, b, c = [x.strip() for x in ln.split(",")]
-                sm.append(float(a))
-                mx = max(mx, float(b))
-                bits = int(c, 16)
-                for i, name in enumerate(REASONS):
-                    if bits & (1 << i) and name != "gpu_idle":
-                        reasons.add(name)
-            except ValueError:
-                continue
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        reasons = set()
+        for _, rs in self.samples:
+            for bit, name in REASONS.items():
+                if rs & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm), "source": "NVML polled every 2 ms in the timed region"}
 
 
 # ----------------------------------------------------------------------------- peaks

@@ -14,7 +14,7 @@ from .errors import (DegenerateGeometryError, EigenSolveError,
                      IndefiniteOperatorError, WQConstructionError)
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmfwq.so")
+LIB_PATH = os.environ.get("MFWQ_LIB") or os.path.join(_PKG, "libmfwq.so")  # override: experiments only
 
 _lib = None
 

@@ -13,13 +13,13 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "mfwq")
-LIB = os.path.join(PKG, "libmfwq.so")
+BUILD = os.path.join(ROOT, "build", os.environ.get("MFWQ_BUILD_TAG", "mfwq"))
+LIB = os.environ.get("MFWQ_BUILD_LIB") or os.path.join(PKG, "libmfwq.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["rule1d.cpp", "stiffness.cu", "fused_matvec.cu", "fd.cu", "pcg.cu", "capi.cu"]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC] + os.environ.get("MFWQ_NVCC_EXTRA", "").split()
+SOURCES = ["rule1d.cpp", "stiffness.cu", "fused_matvec.cu", "fused2.cu", "fd.cu", "pcg.cu", "capi.cu"]
 LIBS = ["-lcusolver", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64"]
 
 

@@ -146,7 +146,7 @@ int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x, double* y, void* s
 
 int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path) {
   return guard([&] {
-    if (path < 0 || path > 2) throw ValueErr("path must be 0, 1 or 2");
+    if (path < 0 || path > 3) throw ValueErr("path must be 0..3");
     h->op.path = path;
   });
 }

@@ -39,8 +39,9 @@ class Stiffness {
   bool grid_nonzero[6] = {true, true, true, true, true, true};
   bool coeffs_ready = false;
   long long flops = 0;            // CostMeter count of one apply (kron.py:90-96)
-  int path = 0;                   // 0 = auto, 1 = generic (K1), 2 = fused
+  int path = 0;                   // 0 = auto/fused v2, 1 = generic (K1), 2 = fused v2, 3 = fused v1
   StencilInfo stencil;
+  std::shared_ptr<void> fused_plan, fused2_plan;  // element-blocked tables + tiles of the fused kernel
   long long nnz_[3][6] = {};      // interior-restricted nnz per direction: B0,B1,W00,W01,W10,W11
 
   // generic-path scratch

@@ -128,8 +128,8 @@ class StiffnessOperator:
         return out
 
     def set_path(self, path: str):
-        """'auto' | 'generic' | 'fused' kernel path (all on the GPU)."""
-        _lib.check(_lib.lib().mfwq_stiffness_set_path(self._h, {"auto": 0, "generic": 1, "fused": 2}[path]))
+        """'auto' | 'generic' | 'fused' | 'fused_v1' kernel path (all on the GPU)."""
+        _lib.check(_lib.lib().mfwq_stiffness_set_path(self._h, {"auto": 0, "generic": 1, "fused": 2, "fused_v1": 3}[path]))
 
     def info(self):
         tm, so, dev = C.c_int(), C.c_int(), C.c_double()

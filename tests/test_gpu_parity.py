@@ -155,4 +155,4 @@ def test_torch_device_inputs_stay_on_device():
     x = torch.randn(space.n_dofs, dtype=torch.float64, device="cuda")
     y = A.apply(x)
     assert isinstance(y, torch.Tensor) and y.is_cuda
-    assert relerr(y.cpu().numpy(), A.apply(x.cpu().numpy())) == 0.0
+    assert relerr(y.cpu().numpy(), A.apply(x.cpu().numpy())) <= 1e-14  # fp64 atomics: order-dependent rounding
