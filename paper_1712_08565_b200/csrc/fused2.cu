@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 
 #include "ops.h"
 
@@ -124,9 +125,10 @@ __host__ __device__ constexpr bool ytype_used(int w) {
 
 // ---- PTX helpers -------------------------------------------------------------
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+  // not volatile: independent MMAs of different tiles may be interleaved by the scheduler
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -161,13 +163,65 @@ template <int P, int NT>
 struct Occ {  // 2 CTAs/SM where the register budget allows it
   static constexpr int MINB = ((NT == 3 && P <= 6) || (NT == 5 && P <= 2)) ? 2 : 1;
 };
+template <int NT>
+__host__ __device__ constexpr int n_xtypes() {
+  int n = 0;
+  for (int w = 0; w < 4; ++w) {
+    bool u = false;
+    for (int t = 0; t < NT; ++t) u = u || wtype(Terms<NT>::a(t), Terms<NT>::b(t), 0) == w;
+    n += u ? 1 : 0;
+  }
+  return n;
+}
+template <int NT>
+__host__ __device__ constexpr int xslot(int w) {  // compact index of x-type w among used x-types
+  int n = 0;
+  for (int v = 0; v < w; ++v) {
+    bool u = false;
+    for (int t = 0; t < NT; ++t) u = u || wtype(Terms<NT>::a(t), Terms<NT>::b(t), 0) == v;
+    n += u ? 1 : 0;
+  }
+  return n;
+}
+template <int NT>
+__host__ __device__ constexpr int n_ytypes() {
+  int n = 0;
+  for (int w = 0; w < 4; ++w) n += ytype_used<NT>(w) ? 1 : 0;
+  return n;
+}
+template <int NT>
+__host__ __device__ constexpr int yslot(int w) {
+  int n = 0;
+  for (int v = 0; v < w; ++v) n += ytype_used<NT>(v) ? 1 : 0;
+  return n;
+}
 
-template <int P, int NT>
+// shared-memory plan (doubles), shared by kernel and host launch code
+template <int P, int NT, int ZS>
+struct Smem {
+  static constexpr int NB = P + 1, NW = P + 2;
+  static constexpr int NBP = (NB + 1) & ~1, NWP = (NW + 1) & ~1;  // 16-byte aligned sub-tables
+  static constexpr int ZT = 2 * NBP + 4 * NWP;                     // z-table doubles per plane
+  static constexpr int G = n_grids<NT>(), NX = n_xtypes<NT>(), NY = n_ytypes<NT>();
+  static constexpr int CST = ZS * 2 * G * 256;                      // one TMA stage
+  static constexpr int TSZ = ZS * NT * TQ * PK;                     // sT (aliases the consumed C stage)
+  static constexpr int ASZ = ZS * 2 * TQ * PV, SSZ = ZS * NT * TQ * PV;
+  static constexpr int AS = ASZ > SSZ ? ASZ : SSZ;                  // sA / sS union
+  static_assert(TSZ <= CST, "sT must fit in a coefficient stage");
+  static constexpr int oC = 0, oBy = 2 * CST, oWx = oBy + 2 * TQ * PKB, oWy = oWx + NX * TQ * PV,
+                       oV = oWy + NY * PV * PK, oAS = oV + ZS * PV * PV, oBx = oAS + AS, oZ = oBx + 2 * TQ * NB;
+  static size_t bytes(int qe, int max_chunk) {
+    return sizeof(double) * (size_t)(oZ + 2 * ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + sizeof(int) * (max_chunk + 2);
+  }
+};
+
+template <int P, int NT, int ZS>
 __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     k_fused(const __grid_constant__ Params prm, const __grid_constant__ Maps maps) {
-  constexpr int NB = P + 1, NW = P + 2;
-  constexpr int ZT = 2 * NB + 4 * NW;            // z-table doubles per quadrature plane
-  constexpr int G = n_grids<NT>();
+  using L = Smem<P, NT, ZS>;
+  constexpr int NB = L::NB, NW = L::NW, NBP = L::NBP, NWP = L::NWP, ZT = L::ZT, G = L::G;
+  constexpr int R = NB + ZS - 1;                 // ring slots (B side)
+  constexpr int A = NW + ZS - 1;                 // accumulator slots (W side)
   constexpr int DMAX = TQ / 2 + P + 1;           // DoF window bound (8 elements + p + 1)
   constexpr int NTD = (DMAX + 7) / 8;            // 8-wide tiles over a window dimension
   constexpr int KB = ((DMAX + 3) / 4);           // k-steps over window rows (By)
@@ -176,20 +230,19 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 
   const int QE = prm.qe;  // max quadrature planes per z-element
   extern __shared__ __align__(128) double sm[];
-  double* sC = sm;                                  // [2][G][2][16*16] TMA stages (2 q-planes)
-  double* sBy = sC + 4 * G * 256;                   // [2][16][PKB]    dense By(q2, r)
-  double* sWxT = sBy + 2 * TQ * PKB;                // [4][16][PV]     dense Wx^T(ql, c)
-  double* sWy = sWxT + 4 * TQ * PV;                 // [4][PV][PK]     dense Wy(r, q2)
-  double* sV = sWy + 4 * PV * PK;                   // [2][PV][PV]     v plane windows
-  double* sA = sV + 2 * PV * PV;                    // [2][16][PV]     B-side y result
-  double* sT = sA + 2 * TQ * PV;                    // [NT][16][PK]    completed z rows
-  double* sS = sT + NT * TQ * PK;                   // [NT][16][PV]    W x results
-  double* sBx = sS + NT * TQ * PV;                  // [2][16][NB]
-  double* sZ = sBx + 2 * TQ * NB;                   // [2][QE][ZT]     z tables of one element
-  int* sEx = reinterpret_cast<int*>(sZ + 2 * QE * ZT);  // [16]
-  int* sEy = sEx + TQ;                              // [16]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sEy + TQ);  // [2]
-  int* sQ0 = reinterpret_cast<int*>(mbar + 2);      // chunk element -> first q (nez+1)
+  double* sC = sm + L::oC;       // [2][ZS*2 planes][G][256]  TMA stages
+  double* sBy = sm + L::oBy;     // [2][16][PKB]              dense By(q2, r)
+  double* sWxT = sm + L::oWx;    // [NX][16][PV]              dense Wx^T(ql, c), used x-types
+  double* sWy = sm + L::oWy;     // [NY][PV][PK]              dense Wy(r, q2), used y-types
+  double* sV = sm + L::oV;       // [ZS][PV][PV]              v plane windows
+  double* sA = sm + L::oAS;      // [ZS][2][16][PV]           B-side y result   (union with sS)
+  double* sS = sm + L::oAS;      // [ZS][NT][16][PV]          W x results
+  double* sBx = sm + L::oBx;     // [2][16][NB]
+  double* sZ = sm + L::oZ;       // [2][ZS*QE][ZT]            z tables
+  int* sEx = reinterpret_cast<int*>(sZ + 2 * ZS * QE * ZT);
+  int* sEy = sEx + TQ;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sEy + TQ);
+  int* sQ0 = reinterpret_cast<int*>(mbar + 2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ql1 = tid & 15, ql2 = tid >> 4;
@@ -215,55 +268,70 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
-  for (int i = tid; i < 2 * PV * PV; i += NTHR) sV[i] = 0.0;
+  for (int i = tid; i < ZS * PV * PV; i += NTHR) sV[i] = 0.0;
   __syncthreads();
-  const double* __restrict__ Bx = prm.B[0];
-  const double* __restrict__ By = prm.B[1];
-  const double* __restrict__ Wx = prm.W[0];
-  const double* __restrict__ Wy = prm.W[1];
-  for (int i = tid; i < 2 * TQ * PKB; i += NTHR) {  // By(q2, r) = Bt[b][q2][r - e(q2) - 1]
-    const int b = i / (TQ * PKB), q = (i / PKB) % TQ, r = i % PKB;
-    const int k = r - sEy[q] - 1;
-    sBy[i] = (q < Ty && k >= 0 && k < NB) ? By[((size_t)b * m2 + ty.q0 + q) * NB + k] : 0.0;
-  }
-  for (int i = tid; i < 4 * TQ * PV; i += NTHR) {  // Wx^T(ql, c) = Wt[w][ql][c - e(ql)]
-    const int w = i / (TQ * PV), q = (i / PV) % TQ, c = i % PV;
-    const int k = c - sEx[q];
-    sWxT[i] = (q < Tx && k >= 0 && k < NW) ? Wx[((size_t)w * m1 + tx.q0 + q) * NW + k] : 0.0;
-  }
-  for (int i = tid; i < 4 * PV * PK; i += NTHR) {  // Wy(r, q2) = Wt[w][q2][r - e(q2)]
-    const int w = i / (PV * PK), r = (i / PK) % PV, q = i % PK;
-    const int k = q < TQ ? r - sEy[q] : -1;
-    sWy[i] = (q < Ty && k >= 0 && k < NW) ? Wy[((size_t)w * m2 + ty.q0 + q) * NW + k] : 0.0;
-  }
-  for (int i = tid; i < 2 * TQ * NB; i += NTHR) {
-    const int b = i / (TQ * NB), q = (i / NB) % TQ, k = i % NB;
-    sBx[i] = q < Tx ? Bx[((size_t)b * m1 + tx.q0 + q) * NB + k] : 0.0;
+  {
+    const double* __restrict__ Bx = prm.B[0];
+    const double* __restrict__ By = prm.B[1];
+    const double* __restrict__ Wx = prm.W[0];
+    const double* __restrict__ Wy = prm.W[1];
+    for (int i = tid; i < 2 * TQ * PKB; i += NTHR) {  // By(q2, r) = Bt[b][q2][r - e(q2) - 1]
+      const int b = i / (TQ * PKB), q = (i / PKB) % TQ, r = i % PKB;
+      const int k = r - sEy[q] - 1;
+      sBy[i] = (q < Ty && k >= 0 && k < NB) ? By[((size_t)b * m2 + ty.q0 + q) * NB + k] : 0.0;
+    }
+    for (int w = 0; w < 4; ++w) {
+      bool xu = false, yu = false;
+      int xs = 0, ys = 0;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (v == w) {
+          xu = xslot<NT>(v + 1) > xslot<NT>(v);  // x-type v used by some term
+          yu = ytype_used<NT>(v);
+          xs = xslot<NT>(v);
+          ys = yslot<NT>(v);
+        }
+      if (xu)
+        for (int i = tid; i < TQ * PV; i += NTHR) {  // Wx^T(ql, c) = Wt[w][ql][c - e(ql)]
+          const int q = i / PV, c = i % PV, k = c - sEx[q];
+          sWxT[xs * TQ * PV + i] = (q < Tx && k >= 0 && k < NW) ? Wx[((size_t)w * m1 + tx.q0 + q) * NW + k] : 0.0;
+        }
+      if (yu)
+        for (int i = tid; i < PV * PK; i += NTHR) {  // Wy(r, q2) = Wt[w][q2][r - e(q2)]
+          const int r = i / PK, q = i % PK;
+          const int k = q < TQ ? r - sEy[q] : -1;
+          sWy[ys * PV * PK + i] = (q < Ty && k >= 0 && k < NW) ? Wy[((size_t)w * m2 + ty.q0 + q) * NW + k] : 0.0;
+        }
+    }
+    for (int i = tid; i < 2 * TQ * NB; i += NTHR) {
+      const int b = i / (TQ * NB), q = (i / NB) % TQ, k = i % NB;
+      sBx[i] = q < Tx ? Bx[((size_t)b * m1 + tx.q0 + q) * NB + k] : 0.0;
+    }
   }
   __syncthreads();
 
   const bool active = ql1 < Tx && ql2 < Ty;
   const int ex = sEx[ql1];
   PROF_DECL
-  double hx[NB], hy[NB], h0[NB];
+  double hx[R], hy[R], h0[R];
 #pragma unroll
-  for (int k = 0; k < NB; ++k) hx[k] = hy[k] = h0[k] = 0.0;
-  double acc[NT][NW];
+  for (int k = 0; k < R; ++k) hx[k] = hy[k] = h0[k] = 0.0;
+  double acc[NT][A];
 #pragma unroll
   for (int t = 0; t < NT; ++t)
 #pragma unroll
-    for (int k = 0; k < NW; ++k) acc[t][k] = 0.0;
+    for (int k = 0; k < A; ++k) acc[t][k] = 0.0;
 
   const double* __restrict__ xv = prm.x;
   double* __restrict__ yv = prm.y;
   const double* __restrict__ ZB = prm.B[2];
   const double* __restrict__ ZW = prm.W[2];
 
-  // v-plane window -> sV[buf] (cp.async, zero fill outside the domain); no commit
-  auto fetch_plane = [&](int i3, int buf) {
+  // v-plane window -> sV[z] (cp.async, zero fill outside the domain); caller commits
+  auto fetch_plane = [&](int i3, int z) {
     if (MFWQ_ABLATE == 5) return;
     const bool vp = i3 >= 0 && i3 < n3;
-    double* dst = sV + buf * PV * PV;
+    double* dst = sV + z * PV * PV;
     for (int r = warp; r < Dy; r += NWARP) {
       const int g2 = day + r;
       const bool rok = vp && g2 >= 0 && g2 < n2;
@@ -275,57 +343,64 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       }
     }
   };
-  // z tables of chunk element el (local) -> sZ[buf]
-  auto fetch_ztab = [&](int el, int buf) {
+  // z tables of chunk elements [el, el+ZS) -> sZ[stage] (plane rows ez*QE + zl)
+  auto fetch_ztab = [&](int el, int stage) {
     if (MFWQ_ABLATE == 6) return;
-    const int qa = sQ0[el], nq = sQ0[el + 1] - qa;
-    double* dst = sZ + buf * QE * ZT;
-    for (int i = tid; i < nq * ZT; i += NTHR) {
-      const int zl = i / ZT, j = i % ZT;
-      const double* src = j < 2 * NB ? ZB + ((size_t)(j / NB) * m3 + qa + zl) * NB + j % NB
-                                     : ZW + ((size_t)((j - 2 * NB) / NW) * m3 + qa + zl) * NW + (j - 2 * NB) % NW;
-      cp_async8(dst + i, src, true);
+    double* dst = sZ + stage * ZS * QE * ZT;
+#pragma unroll
+    for (int ez = 0; ez < ZS; ++ez) {
+      if (el + ez >= nez) break;
+      const int qa = sQ0[el + ez], nq = sQ0[el + ez + 1] - qa;
+      for (int i = tid; i < nq * ZT; i += NTHR) {
+        const int zl = i / ZT, j = i % ZT;
+        const double* src;
+        bool ok = true;
+        if (j < 2 * NBP) {
+          const int b = j / NBP, k = j % NBP;
+          ok = k < NB;
+          src = ZB + ((size_t)b * m3 + qa + zl) * NB + (ok ? k : 0);
+        } else {
+          const int w = (j - 2 * NBP) / NWP, k = (j - 2 * NBP) % NWP;
+          ok = k < NW;
+          src = ZW + ((size_t)w * m3 + qa + zl) * NW + (ok ? k : 0);
+        }
+        cp_async8(dst + (ez * QE + zl) * ZT + j, src, ok);
+      }
     }
   };
-  // coefficient planes of chunk element el (2 quadrature planes) -> sC[stage] by TMA
+  // coefficient planes of chunk elements [el, el+ZS) (2 planes each) -> sC[stage] by TMA
   auto issue_coeff = [&](int el, int stage) {
     if (tid == 0) {
-      const int qa = sQ0[el];
-      mbar_expect_tx(&mbar[stage], G * 2 * bw * bh * 8);
+      mbar_expect_tx(&mbar[stage], ZS * G * 2 * bw * bh * 8);
 #pragma unroll
-      for (int g = 0; g < 6; ++g) {
-        if (!grid_used<NT>(g)) continue;
-        const int sl = grid_slot<NT>(g);
-        tma_load_3d(sC + ((stage * G + sl) * 2 + 0) * 256, &maps.m[var][g], tx.q0, ty.q0, qa, &mbar[stage]);
-        tma_load_3d(sC + ((stage * G + sl) * 2 + 1) * 256, &maps.m[var][g], tx.q0, ty.q0, qa + 1, &mbar[stage]);
+      for (int ez = 0; ez < ZS; ++ez) {
+        const int qa = sQ0[el + ez];
+#pragma unroll
+        for (int g = 0; g < 6; ++g) {
+          if (!grid_used<NT>(g)) continue;
+          const int sl = grid_slot<NT>(g);
+#pragma unroll
+          for (int pl = 0; pl < 2; ++pl)
+            tma_load_3d(sC + stage * L::CST + ((ez * 2 + pl) * G + sl) * 256, &maps.m[var][g], tx.q0, ty.q0,
+                        qa + pl, &mbar[stage]);
+        }
       }
     }
   };
-
-  // B side, in-plane: DMMA y-contraction of sV[buf] -> sA, then per-thread x -> ring
-  auto bside = [&](int buf) {
-    const double* V = sV + buf * PV * PV;
-    for (int task = warp; task < (MFWQ_ABLATE == 2 ? 0 : 2 * 2 * NTD); task += NWARP) {  // (b, mt over q2, nt over c)
-      const int b = task / (2 * NTD), mt = (task / NTD) % 2, nt = task % NTD;
-      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      const double* ap = sBy + (b * TQ + mt * 8 + (lane >> 2)) * PKB + (lane & 3);
-      const double* bp = V + (lane & 3) * PV + nt * 8 + (lane >> 2);
+  auto all_two = [&](int el) {  // every element of the step has exactly 2 quadrature planes
+    bool ok = true;
 #pragma unroll
-      for (int ks = 0; ks < KB; ks += 2) {
-        dmma(d0, d1, ap[ks * 4], bp[ks * 4 * PV]);
-        if (ks + 1 < KB) dmma(e0, e1, ap[ks * 4 + 4], bp[(ks * 4 + 4) * PV]);
-      }
-      double* o = sA + (b * TQ + mt * 8 + (lane >> 2)) * PV + nt * 8 + 2 * (lane & 3);
-      o[0] = d0 + e0;
-      o[1] = d1 + e1;
-    }
-    __syncthreads();
-    PROF(2)
+    for (int ez = 0; ez < ZS; ++ez) ok = ok && (el + ez < nez) && (sQ0[el + ez + 1] - sQ0[el + ez] == 2);
+    return ok;
+  };
+
+  // push one DoF plane (already contracted in y into sA[z]) through the x-contraction into the ring
+  auto push_x = [&](int z) {
     double vx = 0.0, vy = 0.0, v0 = 0.0;
-    const double* a0 = sA + ql2 * PV + ex + 1;
-    const double* a1 = sA + (TQ + ql2) * PV + ex + 1;
+    const double* a0 = sA + (z * 2 * TQ + ql2) * PV + ex + 1;
+    const double* a1 = a0 + TQ * PV;
     const double* b0 = sBx + ql1 * NB;
-    const double* b1 = sBx + (TQ + ql1) * NB;
+    const double* b1 = b0 + TQ * NB;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       const double c0 = b0[k], c1 = b1[k], x0 = a0[k];
@@ -334,58 +409,99 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       vy = fma(c0, a1[k], vy);
     }
 #pragma unroll
-    for (int k = 0; k < NB - 1; ++k) {
+    for (int k = 0; k < R - 1; ++k) {
       hx[k] = hx[k + 1];
       hy[k] = hy[k + 1];
       h0[k] = h0[k + 1];
     }
-    hx[NB - 1] = vx;
-    hy[NB - 1] = vy;
-    h0[NB - 1] = v0;
+    hx[R - 1] = vx;
+    hy[R - 1] = vy;
+    h0[R - 1] = v0;
+  };
+  // B side, in-plane: DMMA y-contraction of nz planes of sV -> sA
+  auto bside_y = [&](int nz) {
+    for (int task = warp; task < (MFWQ_ABLATE == 2 ? 0 : 2 * 2 * NTD); task += NWARP) {  // (b, mt, nt)
+      const int b = task / (2 * NTD), mt = (task / NTD) % 2, nt = task % NTD;
+      const double* ap = sBy + (b * TQ + mt * 8 + (lane >> 2)) * PKB + (lane & 3);
+      double a[KB];
+#pragma unroll
+      for (int ks = 0; ks < KB; ++ks) a[ks] = ap[ks * 4];  // A fragments shared by the planes
+#pragma unroll
+      for (int z = 0; z < ZS; ++z) {
+        if (z >= nz) break;
+        const double* bp = sV + z * PV * PV + (lane & 3) * PV + nt * 8 + (lane >> 2);
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KB; ks += 2) {
+          dmma(d0, d1, a[ks], bp[ks * 4 * PV]);
+          if (ks + 1 < KB) dmma(e0, e1, a[ks + 1], bp[(ks * 4 + 4) * PV]);
+        }
+        double* o = sA + ((z * 2 + b) * TQ + mt * 8 + (lane >> 2)) * PV + nt * 8 + 2 * (lane & 3);
+        o[0] = d0 + e0;
+        o[1] = d1 + e1;
+      }
+    }
   };
 
-  // W side: emit accumulator slot 0 as interior DoF plane i3, shift the window
-  auto emit = [&](int i3) {
+  // W side: emit accumulator slots 0..ne-1 as interior DoF planes i3s, i3s+1, ...; shift by ne
+  auto emit_rows = [&](auto NEc, double* sT, int i3s) {
+    constexpr int ne = decltype(NEc)::value;  // rows emitted (ZS in the main loop, 1 in tail/flush)
+    // sT must not be in use by anyone (caller syncs)
+    double* st = sT + ql2 * PK + ql1;
 #pragma unroll
-    for (int t = 0; t < NT; ++t) sT[(t * TQ + ql2) * PK + ql1] = active ? acc[t][0] : 0.0;
+    for (int z = 0; z < ne; ++z)
+#pragma unroll
+      for (int t = 0; t < NT; ++t) st[(z * NT + t) * TQ * PK] = active ? acc[t][z] : 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
 #pragma unroll
-      for (int k = 0; k < NW - 1; ++k) acc[t][k] = acc[t][k + 1];
-      acc[t][NW - 1] = 0.0;
+      for (int k = 0; k < A - ne; ++k) acc[t][k] = acc[t][k + ne];
+#pragma unroll
+      for (int k = A - ne; k < A; ++k) acc[t][k] = 0.0;
     }
-    if (i3 < 0 || i3 >= n3) return;  // CTA-uniform
-    PROF(5)
-#if MFWQ_ABLATE == 1
-    return;  // timing experiment only: skip the in-plane W contractions
-#endif
+    if (i3s + ne - 1 < 0 || i3s >= n3) return;  // no valid row (CTA-uniform)
     __syncthreads();
     PROF(6)
-    // x-contraction per term: S_t(q2, c) = sum_ql T_t(q2, ql) Wx_t^T(ql, c)
-    for (int task = warp; task < NT * 2 * NTD; task += NWARP) {
-      const int t = task / (2 * NTD), mt = (task / NTD) % 2, nt = task % NTD;
-      int wx = 0;
+#if MFWQ_ABLATE == 1
+    return;
+#endif
+    // x-contraction per (row, term): S(q2, c) = sum_ql T(q2, ql) Wx^T(ql, c)
+    {
+      constexpr int NTASK = ne * NT * 2 * NTD, PER = (NTASK + NWARP - 1) / NWARP;
+      double d[PER][4];
 #pragma unroll
-      for (int u = 0; u < NT; ++u)
-        if (u == t) wx = wtype(T::a(u), T::b(u), 0);
-      const double* ap = sT + (t * TQ + mt * 8 + (lane >> 2)) * PK + (lane & 3);
-      const double* bp = sWxT + (wx * TQ + (lane & 3)) * PV + nt * 8 + (lane >> 2);
-      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      dmma(d0, d1, ap[0], bp[0]);
-      dmma(e0, e1, ap[4], bp[4 * PV]);
-      dmma(d0, d1, ap[8], bp[8 * PV]);
-      dmma(e0, e1, ap[12], bp[12 * PV]);
-      double* o = sS + (t * TQ + mt * 8 + (lane >> 2)) * PV + nt * 8 + 2 * (lane & 3);
-      o[0] = d0 + e0;
-      o[1] = d1 + e1;
+      for (int i = 0; i < PER; ++i) {  // independent tiles per warp, interleaved
+        const int task = warp + i * NWARP;
+        d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0;
+        if (NTASK % NWARP != 0 && task >= NTASK) continue;
+        const int z = task / (NT * 2 * NTD), t = (task / (2 * NTD)) % NT, mt = (task / NTD) % 2, nt = task % NTD;
+        int xs = 0;
+#pragma unroll
+        for (int u = 0; u < NT; ++u)
+          if (u == t) xs = xslot<NT>(wtype(T::a(u), T::b(u), 0));
+        const double* ap = sT + ((z * NT + t) * TQ + mt * 8 + (lane >> 2)) * PK + (lane & 3);
+        const double* bp = sWxT + (xs * TQ + (lane & 3)) * PV + nt * 8 + (lane >> 2);
+        dmma(d[i][0], d[i][1], ap[0], bp[0]);
+        dmma(d[i][2], d[i][3], ap[4], bp[4 * PV]);
+        dmma(d[i][0], d[i][1], ap[8], bp[8 * PV]);
+        dmma(d[i][2], d[i][3], ap[12], bp[12 * PV]);
+      }
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int task = warp + i * NWARP;
+        if (NTASK % NWARP != 0 && task >= NTASK) continue;
+        const int z = task / (NT * 2 * NTD), t = (task / (2 * NTD)) % NT, mt = (task / NTD) % 2, nt = task % NTD;
+        double* o = sS + ((z * NT + t) * TQ + mt * 8 + (lane >> 2)) * PV + nt * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(o) = make_double2(d[i][0] + d[i][2], d[i][1] + d[i][3]);
+      }
     }
     __syncthreads();
     PROF(7)
-    // y-contraction, summed over y-factor groups inside the K loop:
-    //   out(r, c) = sum_w sum_q2 Wy_w(r, q2) * sum_{t: ytype(t)=w} S_t(q2, c)
-    const size_t plane = (size_t)i3 * n2;
-    for (int task = warp; task < NTD * NTD; task += NWARP) {
-      const int mt = task / NTD, nt = task % NTD;
+    // y-contraction, summed over y-factor groups inside the K loop, then atomics
+    for (int task = warp; task < ne * NTD * NTD; task += NWARP) {
+      const int z = task / (NTD * NTD), mt = (task / NTD) % NTD, nt = task % NTD;
+      const int i3 = i3s + z;
+      if (i3 < 0 || i3 >= n3) continue;
       double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
       int chain = 0;
 #pragma unroll
@@ -394,11 +510,11 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const int kq = ks * 4 + (lane & 3);
-          const double a = sWy[(w * PV + mt * 8 + (lane >> 2)) * PK + kq];
+          const double a = sWy[(yslot<NT>(w) * PV + mt * 8 + (lane >> 2)) * PK + kq];
           double bb = 0.0;
 #pragma unroll
           for (int t = 0; t < NT; ++t)
-            if (wtype(T::a(t), T::b(t), 1) == w) bb += sS[(t * TQ + kq) * PV + nt * 8 + (lane >> 2)];
+            if (wtype(T::a(t), T::b(t), 1) == w) bb += sS[((z * NT + t) * TQ + kq) * PV + nt * 8 + (lane >> 2)];
           if (chain++ & 1) dmma(e0, e1, a, bb);
           else dmma(d0, d1, a, bb);
         }
@@ -407,6 +523,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       d1 += e1;
       const int r = mt * 8 + (lane >> 2), c = nt * 8 + 2 * (lane & 3);
       const int g2 = day + r, g1 = dax + c;
+      const size_t plane = (size_t)i3 * n2;
       if (r < Dy && g2 >= 0 && g2 < n2) {
 #if MFWQ_ABLATE == 4  // timing experiment only: plain stores instead of atomics
         if (c < Dx && g1 >= 0 && g1 < n1) yv[(plane + g2) * n1 + g1] = d0;
@@ -417,41 +534,64 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #endif
       }
     }
-    __syncthreads();  // sT / sS free for the next row
     PROF(8)
   };
 
-  // z-part for local plane zl of the element whose tables sit in sZ[zbuf]
-  auto zpoint = [&](int qz, int zl, const double* zt, const double* cst, int pl) {
-    const double* zb0 = zt + zl * ZT;
-    const double* zb1 = zb0 + NB;
-    const double* zw = zb0 + 2 * NB;
+  // z-part for one quadrature plane: ring offset ro, accumulator offset ez.
+  // TMAc: coefficients from the TMA stage (cst) or straight from global memory.
+  auto zpoint = [&](auto TMAc, int qz, int ro, int ez, const double* zrow, const double* cst) {
+    constexpr bool kTMA = decltype(TMAc)::value;
+    const double2* zb0 = reinterpret_cast<const double2*>(zrow);
+    const double2* zb1 = reinterpret_cast<const double2*>(zrow + NBP);
+    const double2* zw = reinterpret_cast<const double2*>(zrow + 2 * NBP);
     double gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      const double c0 = zb0[k];
-      gx = fma(c0, hx[k], gx);
-      gy = fma(c0, hy[k], gy);
-      gz = fma(zb1[k], h0[k], gz);
+    for (int k2 = 0; k2 < NBP / 2; ++k2) {
+      const double2 c0 = zb0[k2], c1 = zb1[k2];
+      const int k = 2 * k2;
+      gx = fma(c0.x, hx[ro + k], gx);
+      gy = fma(c0.x, hy[ro + k], gy);
+      gz = fma(c1.x, h0[ro + k], gz);
+      if (k + 1 < NB) {
+        gx = fma(c0.y, hx[ro + k + 1], gx);
+        gy = fma(c0.y, hy[ro + k + 1], gy);
+        gz = fma(c1.y, h0[ro + k + 1], gz);
+      }
     }
     if (!active || MFWQ_ABLATE == 3) return;
     double cg[6];
 #pragma unroll
     for (int g = 0; g < 6; ++g) {
       if (!grid_used<NT>(g)) { cg[g] = 0.0; continue; }
-      if (cst) cg[g] = cst[(grid_slot<NT>(g) * 2 + pl) * 256 + ql2 * bw + ql1];
+      if constexpr (kTMA) cg[g] = cst[grid_slot<NT>(g) * 256];
       else cg[g] = __ldg(prm.C + g * prm.gstride + ((size_t)qz * m2 + ty.q0 + ql2) * prm.m1p + tx.q0 + ql1);
     }
+    double tv[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int b = T::b(t);
-      const double gb = b == 0 ? gx : (b == 1 ? gy : gz);
-      const double tv = cg[gkey(T::a(t), b)] * gb;
-      const double* wz = zw + wtype(T::a(t), b, 2) * NW;
+      tv[t] = cg[gkey(T::a(t), b)] * (b == 0 ? gx : (b == 1 ? gy : gz));
+    }
 #pragma unroll
-      for (int k = 0; k < NW; ++k) acc[t][k] = fma(wz[k], tv, acc[t][k]);
+    for (int w = 0; w < 4; ++w) {
+      bool used = false;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) used |= wtype(T::a(t), T::b(t), 2) == w;
+      if (!used) continue;
+#pragma unroll
+      for (int k2 = 0; k2 < NWP / 2; ++k2) {
+        const double2 c = zw[w * (NWP / 2) + k2];
+        const int k = 2 * k2;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (wtype(T::a(t), T::b(t), 2) != w) continue;
+          acc[t][ez + k] = fma(c.x, tv[t], acc[t][ez + k]);
+          if (k + 1 < NW) acc[t][ez + k + 1] = fma(c.y, tv[t], acc[t][ez + k + 1]);
+        }
+      }
     }
   };
+  const int cthr = ql2 * bw + ql1;  // this thread's point inside a TMA coefficient box
 
   // ---- prologue: fill the ring with planes ea-1 .. ea+p-2 ----------------------
   for (int k = 0; k < P; ++k) {
@@ -459,48 +599,76 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     cp_commit();
     cp_wait_all();
     __syncthreads();
-    bside(0);
+    bside_y(1);
     __syncthreads();
+    push_x(0);
   }
-  fetch_plane(tz.ea + P - 1, 0);
-  fetch_ztab(0, 0);
-  cp_commit();
-  if (sQ0[1] - sQ0[0] == 2) issue_coeff(0, 0);
+  // per-step TMA eligibility (every element of the step has exactly 2 planes)
+  auto step_tma = [&](int el) { return el + ZS <= nez && all_two(el); };
+  {
+    const int nz0 = nez >= ZS ? ZS : 1;
+    for (int z = 0; z < nz0; ++z) fetch_plane(tz.ea + P - 1 + z, z);
+    fetch_ztab(0, 0);
+    cp_commit();
+    if (step_tma(0)) issue_coeff(0, 0);
+  }
   unsigned parity[2] = {0u, 0u};
 
-  for (int el = 0; el < nez; ++el) {
+  // one step over NZ (compile-time) z-elements starting at chunk element el, stage s
+  auto do_step = [&](auto NZc, int el, int s) {
+    constexpr int nz = decltype(NZc)::value;
     const int e3 = tz.ea + el;
-    const int s = el & 1;
     cp_wait_all();
-    __syncthreads();  // sV[s], sZ[s] landed; everyone done with step el-1 (stage s^1 reusable)
+    __syncthreads();  // sV, sZ[s] landed; step-1 finished with sC[s^1], sZ[s^1], sT/sS
     PROF(0)
-    if (el + 1 < nez) {
-      fetch_plane(e3 + P, s ^ 1);
-      PROF(9)
-      fetch_ztab(el + 1, s ^ 1);
-      cp_commit();
-      if (sQ0[el + 2] - sQ0[el + 1] == 2) issue_coeff(el + 1, s ^ 1);
+    const int eln = el + nz;
+    const int nzn = (nez - eln) >= ZS ? ZS : 1;
+    if (eln < nez) {
+      fetch_ztab(eln, s ^ 1);
+      if (step_tma(eln)) issue_coeff(eln, s ^ 1);
     }
     PROF(1)
-    bside(s);  // ring: planes e3-1 .. e3+p-1
+    bside_y(nz);
+    __syncthreads();  // sA ready; sV free
+    PROF(2)
+    if (eln < nez)
+      for (int z = 0; z < nzn; ++z) fetch_plane(e3 + nz + P - 1 + z, z);  // next step's planes
+    cp_commit();
+#pragma unroll
+    for (int z = 0; z < nz; ++z) push_x(z);  // ring: planes up to e3+p+nz-2
     PROF(3)
-    const int qa = sQ0[el], nq = sQ0[el + 1] - qa;
-    const double* zt = sZ + s * QE * ZT;
-    if (nq == 2) {
+    constexpr int ro0 = ZS - nz;  // ring offset of the step's first element
+    const double* zt = sZ + s * ZS * QE * ZT;
+    if (nz == ZS && step_tma(el)) {
       mbar_wait(&mbar[s], parity[s]);
       parity[s] ^= 1u;
       PROF(4)
-      const double* cst = sC + s * G * 512;
-      zpoint(qa, 0, zt, cst, 0);
-      zpoint(qa + 1, 1, zt, cst, 1);
-    } else {
-      for (int zl = 0; zl < nq; ++zl) zpoint(qa + zl, zl, zt, nullptr, 0);
+      const double* cst = sC + s * L::CST + cthr;
+#pragma unroll
+      for (int ez = 0; ez < nz; ++ez)
+#pragma unroll
+        for (int pl = 0; pl < 2; ++pl)
+          zpoint(std::true_type{}, 0, ro0 + ez, ez, zt + (ez * QE + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
+    } else {  // boundary z-elements (extra planes) or the odd tail: C straight from global
+#pragma unroll
+      for (int ez = 0; ez < nz; ++ez) {
+        const int qa = sQ0[el + ez], nq = sQ0[el + ez + 1] - qa;
+        for (int zl = 0; zl < nq; ++zl)
+          zpoint(std::false_type{}, qa + zl, ro0 + ez, ez, zt + (ez * QE + zl) * ZT, nullptr);
+      }
     }
-    emit(e3 - 2);  // DoF plane j = e3-1 (full) is complete
-  }
+    PROF(5)
+    __syncthreads();  // all reads of sC[s] done -> it becomes sT
+    emit_rows(std::integral_constant<int, nz>{}, sC + s * L::CST, e3 - 2);  // full rows e3-1.. complete
+  };
+
+  int el = 0, step = 0;
+  for (; el + ZS <= nez; el += ZS, ++step) do_step(std::integral_constant<int, ZS>{}, el, step & 1);
+  if (el < nez) do_step(std::integral_constant<int, 1>{}, el, step & 1);  // odd tail
+  // flush the open planes (partial; neighbours add theirs): slot k holds interior row eb-2+k
   for (int k = 0; k < NW - 1; ++k) {
     __syncthreads();
-    emit(tz.eb - 2 + k);  // open planes (partial; neighbours add theirs)
+    emit_rows(std::integral_constant<int, 1>{}, sC, tz.eb - 2 + k);
   }
   PROF_DUMP
 }
@@ -566,6 +734,7 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
       const long long inplane = (long long)F->ntile[0] * F->ntile[1];
       int chunk = int(std::max<long long>(4, (long long)S.dir[2].n_el * inplane / (148 * 4) + 1));
       chunk = std::min(chunk, 64);
+      chunk += chunk & 1;  // even chunks: steps of two z-elements
       for (int e = 0; e < S.dir[2].n_el; e += chunk) {
         const int b = std::min(S.dir[2].n_el, e + chunk);
         t.push_back({e, b, S.dir[2].elem_q0[e], S.dir[2].elem_q0[b] - S.dir[2].elem_q0[e], 0});
@@ -616,6 +785,7 @@ static void encode_maps(Stiffness& S, Fused2Plan& F) {
 
 template <int P, int NT>
 static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
+  constexpr int ZS = 2;
   using namespace f2;
   encode_maps(S, F);
   Params prm;
@@ -641,12 +811,9 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   prm.n1 = S.dir[0].n;
   prm.n2 = S.dir[1].n;
   prm.n3 = S.dir[2].n;
-  constexpr int NB = P + 1, NW = P + 2, G = n_grids<NT>();
   prm.qe = F.qe;
-  size_t smem = sizeof(double) * (4 * G * 256 + 2 * TQ * PKB + 4 * TQ * PV + 4 * PV * PK + 2 * PV * PV + 2 * TQ * PV +
-                                  NT * TQ * PK + NT * TQ * PV + 2 * TQ * NB + (size_t)2 * F.qe * (2 * NB + 4 * NW)) +
-                sizeof(int) * 2 * TQ + 16 + sizeof(int) * (F.max_chunk + 2);
-  auto kern = k_fused<P, NT>;
+  const size_t smem = Smem<P, NT, ZS>::bytes(F.qe, F.max_chunk);
+  auto kern = k_fused<P, NT, ZS>;
   MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   MFWQ_CUDA(cudaMemsetAsync(y, 0, S.N * sizeof(double), s));
   dim3 grid(F.ntile[0] * F.ntile[1], F.ntile[2]);
