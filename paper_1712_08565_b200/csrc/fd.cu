@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdio>
 
+#include "modal_gemm.h"
 #include "ops.h"
 
 namespace mfwq {
@@ -197,10 +198,15 @@ void FastDiag::init(const int* nn, const double* const* K, const double* const* 
       for (int i = 0; i < nl; ++i)
         for (int k = 0; k < nl; ++k) U_h[l][size_t(i) * nl + k] = Z[size_t(k) * nl + i];
     }
-    std::vector<double> T(size_t(nl) * nl);
+    // device copies with an even, zero-padded pitch (16-byte cp.async of A tiles)
+    const int ld = nl + (nl & 1);
+    std::vector<double> Up(size_t(nl) * ld, 0.0), T(size_t(nl) * ld, 0.0);
     for (int i = 0; i < nl; ++i)
-      for (int k = 0; k < nl; ++k) T[size_t(k) * nl + i] = U_h[l][size_t(i) * nl + k];
-    U[l].upload(U_h[l].data(), U_h[l].size());
+      for (int k = 0; k < nl; ++k) {
+        Up[size_t(i) * ld + k] = U_h[l][size_t(i) * nl + k];
+        T[size_t(k) * ld + i] = U_h[l][size_t(i) * nl + k];
+      }
+    U[l].upload(Up.data(), Up.size());
     Ut[l].upload(T.data(), T.size());
     lam[l].upload(lam_h[l].data(), nl);
   }
@@ -218,20 +224,22 @@ void FastDiag::apply(const double* r, double* z, cudaStream_t s) {
     s1_.alloc(N);
     s2_.alloc(N);
   }
-  gemm::Epi none{nullptr, nullptr, nullptr, 1, 0.0};
-  // direction 1: (n3 n2 x n1) * U1
-  gemm::dgemm(r, U[0].ptr, s1_.ptr, n3 * n2, n1, n1, n1, n1, n1, 1, 0, 0, 0, none, s);
-  // direction 2: per i3, U2^T (n2 x n2) * X (n2 x n1)
-  gemm::dgemm(Ut[1].ptr, s1_.ptr, s2_.ptr, n2, n1, n2, n2, n1, n1, n3, 0, (long long)n2 * n1, (long long)n2 * n1,
-              none, s);
-  // direction 3: U3^T (n3 x n3) * X (n3 x n2 n1), fused 1/(lambda sum) scale
-  gemm::Epi sc{lam[0].ptr, lam[1].ptr, lam[2].ptr, n1, sigma};
-  gemm::dgemm(Ut[2].ptr, s2_.ptr, s1_.ptr, n3, n2 * n1, n3, n3, n2 * n1, n2 * n1, 1, 0, 0, 0, sc, s);
-  // inverse: U3 * Y, per-i3 U2 * Y, Y * U1^T
-  gemm::dgemm(U[2].ptr, s1_.ptr, s2_.ptr, n3, n2 * n1, n3, n3, n2 * n1, n2 * n1, 1, 0, 0, 0, none, s);
-  gemm::dgemm(U[1].ptr, s2_.ptr, s1_.ptr, n2, n1, n2, n2, n1, n1, n3, 0, (long long)n2 * n1, (long long)n2 * n1,
-              none, s);
-  gemm::dgemm(s1_.ptr, Ut[0].ptr, z, n3 * n2, n1, n1, n1, n1, n1, 1, 0, 0, 0, none, s);
+  const long long n12 = (long long)n1 * n2;
+  // mode views of the (n3, n2, n1) tensor: k = contracted index, j = the other two
+  const ModeView vx{1, (long long)n3 * n2, 0, n1};    // k = i1, j = (i3, i2)
+  const ModeView vy{n1, n1, n12, 1};                  // k = i2, j = (i3, i1)
+  const ModeView vz{n12, n12, 0, 1};                  // k = i3, j = (i2, i1)
+  const Scale none{nullptr, nullptr, nullptr, 1, 0.0};
+  const Scale lam_scale{lam[0].ptr, lam[1].ptr, lam[2].ptr, n1, sigma};
+  // forward  (U3 x U2 x U1)^T r, eigenvalue scaling fused into the direction-3 epilogue
+  auto ld = [](int v) { return v + (v & 1); };
+  modal_gemm(Ut[0].ptr, ld(n1), n1, n1, r, vx, s1_.ptr, vx, (long long)n3 * n2, none, true, s);
+  modal_gemm(Ut[1].ptr, ld(n2), n2, n2, s1_.ptr, vy, s2_.ptr, vy, (long long)n3 * n1, none, false, s);
+  modal_gemm(Ut[2].ptr, ld(n3), n3, n3, s2_.ptr, vz, s1_.ptr, vz, n12, lam_scale, false, s);
+  // inverse  (U3 x U2 x U1) y
+  modal_gemm(U[2].ptr, ld(n3), n3, n3, s1_.ptr, vz, s2_.ptr, vz, n12, none, false, s);
+  modal_gemm(U[1].ptr, ld(n2), n2, n2, s2_.ptr, vy, s1_.ptr, vy, (long long)n3 * n1, none, false, s);
+  modal_gemm(U[0].ptr, ld(n1), n1, n1, s1_.ptr, vx, z, vx, (long long)n3 * n2, none, true, s);
 }
 
 }  // namespace mfwq

@@ -1,0 +1,171 @@
+// Modal fp64 tensor-core GEMM for the fast-diagonalisation preconditioner.
+//
+//   C(m, j) = sum_k A[m][k] * X(k, j)      (optionally scaled by 1/(l1+l2+l3+sigma))
+//
+// A is a small dense n x n factor (row-major); X and C are strided "mode views"
+// of an (n3, n2, n1) tensor: element (k, j) lives at k*sk + (j/jdiv)*jhi +
+// (j%jdiv)*jlo, so one kernel applies a 1D factor along any of the three
+// directions (solvers.py:107-115 contracts each direction with kron.py:86-89).
+// The whole mode (n <= 136) is one CTA tile in M, so 130-wide modes waste 4%
+// instead of 32% with square 64x64 tiles.  mma.sync m8n8k4 f64 -> SASS DMMA.
+#include <algorithm>
+
+#include "modal_gemm.h"
+
+namespace mfwq {
+namespace mg {
+
+constexpr int BK = 16, APAD = 4, BPAD = 8, STAGES = 3;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp16(double* dst, const double* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void wait_groups() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ long long colpart(const ModeView& v, long long j) {
+  const unsigned q = (unsigned)j / (unsigned)v.jdiv, r = (unsigned)j - q * (unsigned)v.jdiv;  // N < 2^31
+  return (long long)q * v.jhi + (long long)r * v.jlo;
+}
+
+// MT m8-tiles per warp along M, WM x WN warps, NTW n8-tiles per warp along N.
+template <int MT, int WM, int WN, int NTW, bool KC>
+__global__ void __launch_bounds__(WM * WN * 32, 2)
+    modal_kernel(const double* __restrict__ A, int lda, int M, int K, const double* __restrict__ X, ModeView xv,
+                 double* __restrict__ C, ModeView cv, long long N, Scale sc) {
+  constexpr int BM = 8 * MT * WM;
+  constexpr int THREADS = WM * WN * 32, BN = WN * NTW * 8;
+  constexpr int PA = BK + APAD, PB = BN + BPAD;
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;                          // [STAGES][BM][PA]
+  double* Bs = sm + STAGES * BM * PA;       // [STAGES][BK][PB]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const long long n0 = (long long)blockIdx.x * BN;
+  const int m0 = blockIdx.y * BM;
+
+  // the B-tile columns a thread loads are the same for every k-tile: precompute their offsets
+  constexpr int BPER = (BK * BN) / THREADS;
+  long long bcol[BPER];
+  int brow[BPER], bcc[BPER];
+  bool bok[BPER];
+#pragma unroll
+  for (int i = 0; i < BPER; ++i) {
+    const int e = tid + i * THREADS;
+    if (KC) { bcc[i] = e / BK; brow[i] = e % BK; }  // consecutive lanes walk k (contiguous in memory)
+    else { brow[i] = e / BN; bcc[i] = e % BN; }     // consecutive lanes walk j
+    bok[i] = n0 + bcc[i] < N;
+    bcol[i] = bok[i] ? colpart(xv, n0 + bcc[i]) : 0;
+  }
+  auto load = [&](int stage, int k0) {
+    double* as = As + stage * BM * PA;
+    for (int e = tid; e < BM * (BK / 2); e += THREADS) {  // 16-byte copies: lda even, A zero-padded
+      const int r = e / (BK / 2), c = 2 * (e % (BK / 2)), gm = m0 + r, gk = k0 + c;
+      const bool ok = gm < M && gk < lda;
+      cp16(as + r * PA + c, ok ? A + (long long)gm * lda + gk : A, ok);
+    }
+    double* bs = Bs + stage * BK * PB;
+#pragma unroll
+    for (int i = 0; i < BPER; ++i) {
+      const int gk = k0 + brow[i];
+      const bool ok = bok[i] && gk < K;
+      cp8(bs + brow[i] * PB + bcc[i], ok ? X + (long long)gk * xv.sk + bcol[i] : X, ok);
+    }
+  };
+
+  double acc[MT][NTW][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load(s, s * BK);
+    commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    wait_groups<STAGES - 2>();
+    __syncthreads();
+    {  // prefetch k-tile kt + STAGES - 1 into the slot freed at kt - 1
+      const int kn = kt + STAGES - 1;
+      if (kn < nk) load(kn % STAGES, kn * BK);
+      commit();
+    }
+    const double* as = As + (kt % STAGES) * BM * PA + (wm * MT * 8 + (lane >> 2)) * PA + (lane & 3);
+    const double* bs = Bs + (kt % STAGES) * BK * PB + (lane & 3) * PB + wn * NTW * 8 + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double b[NTW];
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) b[j] = bs[kk * PB + j * 8];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double a = as[i * 8 * PA + kk];
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dmma(acc[i][j][0], acc[i][j][1], a, b[j]);
+      }
+    }
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int m = m0 + (wm * MT + i) * 8 + (lane >> 2);
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NTW; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long col = n0 + (wn * NTW + j) * 8 + 2 * (lane & 3) + h;
+        if (col >= N) continue;
+        double v = acc[i][j][h];
+        if (sc.lam1) {  // solvers.py:93-101: ((l1 + l2) + l3) + sigma
+          double ls = sc.lam1[col % sc.n1] + sc.lam2[col / sc.n1];
+          ls = ls + sc.lam3[m];
+          v = v * (1.0 / (ls + sc.sigma));
+        }
+        C[(long long)m * cv.sk + colpart(cv, col)] = v;
+      }
+  }
+}
+
+template <int MT, int WM, int WN, int NTW>
+static void launch(const double* A, int lda, int M, int K, const double* X, ModeView xv, double* C, ModeView cv,
+                   long long N, Scale sc, bool kc, cudaStream_t s) {
+  constexpr int BM = 8 * MT * WM, THREADS = WM * WN * 32, BN = WN * NTW * 8;
+  const size_t smem = sizeof(double) * STAGES * (BM * (BK + APAD) + BK * (BN + BPAD));
+  dim3 grid((unsigned)((N + BN - 1) / BN), (M + BM - 1) / BM);
+  if (kc) {
+    auto k = modal_kernel<MT, WM, WN, NTW, true>;
+    MFWQ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, THREADS, smem, s>>>(A, lda, M, K, X, xv, C, cv, N, sc); note_launch();
+  } else {
+    auto k = modal_kernel<MT, WM, WN, NTW, false>;
+    MFWQ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, THREADS, smem, s>>>(A, lda, M, K, X, xv, C, cv, N, sc); note_launch();
+  }
+  MFWQ_CUDA(cudaGetLastError());
+}
+
+}  // namespace mg
+
+void modal_gemm(const double* A, int lda, int M, int K, const double* X, ModeView xv, double* C, ModeView cv,
+                long long N, Scale sc, bool kcontig, cudaStream_t s) {
+  // modes up to 144 wide: one 144-row x 32-col tile (2 x 4 warps of 9 m8 x 1 n8); wider: 128-row tiles
+  if (M <= 144) mg::launch<9, 2, 4, 1>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
+  else mg::launch<8, 2, 4, 2>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
+}
+
+}  // namespace mfwq
