@@ -300,6 +300,8 @@ def run_ours(args, rank, world, local):
     pcg = None
     if args.pcg and world == 1:
         pcg = run_pcg(M, torch, dev)
+    elif args.pcg:
+        pcg = run_dist_pcg(M, torch, dev, rank, world)
 
     if rank == 0:
         cpu = None
@@ -327,6 +329,39 @@ def run_ours(args, rank, world, local):
                 "clocks": clk.summary(),
                 "pcg": pcg}
         print(json.dumps(line), flush=True)
+
+
+def run_dist_pcg(M, torch, dev, rank, world):
+    """cfg 3 on `world` GPUs: xi_3 slabs, halo exchange, all-to-all FD, allreduce dots (NCCL)."""
+    import torch.distributed as dist
+    from paper_1712_08565_b200.dist import dist_cg, setup_distributed
+
+    p, n_el = 4, 256
+    space = M.tensor_space(p, n_el)
+    rule = M.build_tensor_rule(space)
+    A, P, part = setup_distributed(space, rule, M.quarter_ring_map())
+    lo, hi = part.owned(rank)
+    plane = A.plane
+    b_full = np.random.default_rng(1).standard_normal(space.n_dofs)
+    b = torch.from_numpy(b_full[lo * plane:hi * plane].copy()).to(dev)
+    dist_cg(A.apply, b, P.apply, tol=1e-8, maxit=2)  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    u, rep = dist_cg(A.apply, b, P.apply, tol=1e-8)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nrm = torch.stack([(u * u).sum()])
+    dist.all_reduce(nrm)
+    secs = float(t)
+    return {"config": f"cfg3 quarter ring p=4 n_el=256, xi3 slabs x{world}", "N": space.n_dofs,
+            "iterations": rep.iterations, "converged": rep.converged, "final_rel_residual": rep.residuals[-1],
+            "solve_s": secs, "dof_iters_per_s": space.n_dofs * rep.iterations / secs,
+            "u_norm": float(nrm[0]) ** 0.5}
 
 
 def run_pcg(M, torch, dev):

@@ -90,7 +90,14 @@ int mfwq_stiffness_get_coeff(mfwq_stiffness_t h, int key, double* out_dev, void*
 int mfwq_stiffness_sizes(mfwq_stiffness_t h, int* n3, int* m3, long long* N, long long* Nq);
 /* y = K x  (device pointers, length N); y is overwritten */
 int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x_dev, double* y_dev, void* stream);
-/* select kernel path: 0 = auto (fused), 1 = generic K1 composition, 2 = fused */
+/* Multi-GPU slab: restrict the operator to z-elements [e_lo, e_hi).
+   Must precede set_geometry/set_coeffs (only the slab's quadrature planes are stored).
+   apply() then maps the input window of interior DoF planes [v_lo, v_hi) to the
+   output window [y_lo, y_hi) (partial sums on the p+1 rows shared with neighbours). */
+int mfwq_stiffness_set_slab(mfwq_stiffness_t h, int e_lo, int e_hi);
+/* info6 = {e_lo, e_hi, v_lo, v_hi, y_lo, y_hi} */
+int mfwq_stiffness_slab_info(mfwq_stiffness_t h, int* info6);
+/* select kernel path: 0 = auto (fused v2), 1 = generic K1 composition, 2 = fused v2, 3 = fused v1 */
 int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path);
 int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* stencil_ok, double* stencil_dev);
 int mfwq_stiffness_flops(mfwq_stiffness_t h, long long* flops);
@@ -103,6 +110,11 @@ typedef struct mfwq_fd_s* mfwq_fd_t;
 /* K3/M3: host row-major (n_l x n_l) interior 1D stiffness / mass per direction */
 int mfwq_fd_create(const int* n3, const double* const* K3, const double* const* M3, double sigma, mfwq_fd_t* out);
 int mfwq_fd_apply(mfwq_fd_t h, const double* r_dev, double* z_dev, void* stream);
+/* one direction of the transform on a local (nz, ny, n1) block, for the multi-GPU
+   slab path: forward applies U_dir^T, inverse U_dir; scale (dir 2, forward) fuses
+   1/(l1[i1] + l2[row_lo + i2] + l3[i3] + sigma).  dir 1 needs ny == n2, dir 2 nz == n3. */
+int mfwq_fd_apply_dir(mfwq_fd_t h, int dir, int inverse, int scale, const double* x_dev, double* y_dev, int nz,
+                      int ny, int row_lo, void* stream);
 /* host copies of eigenvalues (n) and M-orthonormal eigenvectors U (row-major n x n) */
 int mfwq_fd_eigen(mfwq_fd_t h, int dir, double* lam, double* U);
 void mfwq_fd_destroy(mfwq_fd_t h);

@@ -49,6 +49,8 @@ _SIGS = {
     "mfwq_stiffness_sizes": (C.c_int, [C.c_void_p, ip, ip, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "mfwq_stiffness_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mfwq_stiffness_set_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "mfwq_stiffness_set_slab": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "mfwq_stiffness_slab_info": (C.c_int, [C.c_void_p, ip]),
     "mfwq_stiffness_info": (C.c_int, [C.c_void_p, ip, ip, dp]),
     "mfwq_stiffness_flops": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "mfwq_stiffness_flops_active": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
@@ -56,6 +58,8 @@ _SIGS = {
     "mfwq_fd_create": (C.c_int, [ip, C.POINTER(dp), C.POINTER(dp), C.c_double, C.POINTER(C.c_void_p)]),
     "mfwq_fd_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mfwq_fd_eigen": (C.c_int, [C.c_void_p, C.c_int, dp, dp]),
+    "mfwq_fd_apply_dir": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                    C.c_int, C.c_int, C.c_void_p]),
     "mfwq_fd_destroy": (None, [C.c_void_p]),
     "mfwq_pcg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
                                  dp, C.POINTER(KrylovReportC), C.c_void_p]),

@@ -144,6 +144,18 @@ int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x, double* y, void* s
   return guard([&] { h->op.apply(x, y, (cudaStream_t)stream); });
 }
 
+int mfwq_stiffness_set_slab(mfwq_stiffness_t h, int e_lo, int e_hi) {
+  return guard([&] { h->op.set_slab(e_lo, e_hi); });
+}
+
+int mfwq_stiffness_slab_info(mfwq_stiffness_t h, int* info6) {
+  return guard([&] {
+    const Stiffness& S = h->op;
+    const int v[6] = {S.e_lo, S.e_hi, S.v_lo, S.v_hi, S.y_lo, S.y_hi};
+    std::memcpy(info6, v, sizeof v);
+  });
+}
+
 int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path) {
   return guard([&] {
     if (path < 0 || path > 3) throw ValueErr("path must be 0..3");
@@ -184,6 +196,11 @@ int mfwq_fd_create(const int* n3, const double* const* K3, const double* const* 
 
 int mfwq_fd_apply(mfwq_fd_t h, const double* r, double* z, void* stream) {
   return guard([&] { h->fd.apply(r, z, (cudaStream_t)stream); });
+}
+
+int mfwq_fd_apply_dir(mfwq_fd_t h, int dir, int inverse, int scale, const double* x, double* y, int nz, int ny,
+                      int row_lo, void* stream) {
+  return guard([&] { h->fd.apply_dir(dir, inverse, scale, x, y, nz, ny, row_lo, (cudaStream_t)stream); });
 }
 
 int mfwq_fd_eigen(mfwq_fd_t h, int dir, double* lam, double* U) {

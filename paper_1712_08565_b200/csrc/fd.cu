@@ -243,3 +243,31 @@ void FastDiag::apply(const double* r, double* z, cudaStream_t s) {
 }
 
 }  // namespace mfwq
+
+namespace mfwq {
+// Direction `dir` of P^-1 on a local (nz, ny, n1) block: forward applies U_dir^T,
+// inverse applies U_dir; `scale` (direction 3 forward only) fuses
+// 1/(l1[i1] + l2[row_lo + i2] + l3[i3] + sigma).  dir 1 needs ny == n2, dir 2 nz == n3.
+void FastDiag::apply_dir(int dir, int inverse, int scale, const double* x, double* y, int nz, int ny, int row_lo,
+                         cudaStream_t s) {
+  if (dir < 0 || dir > 2) throw ValueErr("direction out of range");
+  const int n1 = n[0];
+  if ((dir == 1 && ny != n[1]) || (dir == 2 && nz != n[2])) throw ValueErr("block does not span the direction");
+  if (scale && (dir != 2 || inverse)) throw ValueErr("the eigenvalue scale belongs to the forward direction-3 step");
+  const long long plane = (long long)ny * n1;
+  const double* A = inverse ? U[dir].ptr : Ut[dir].ptr;
+  const int nl = n[dir], ld = nl + (nl & 1);
+  Scale sc{nullptr, nullptr, nullptr, 1, 0.0};
+  if (scale) sc = Scale{lam[0].ptr, lam[1].ptr + row_lo, lam[2].ptr, n1, sigma};
+  if (dir == 0) {
+    const ModeView v{1, (long long)nz * ny, 0, n1};
+    modal_gemm(A, ld, nl, nl, x, v, y, v, (long long)nz * ny, sc, true, s);
+  } else if (dir == 1) {
+    const ModeView v{n1, n1, plane, 1};
+    modal_gemm(A, ld, nl, nl, x, v, y, v, (long long)nz * n1, sc, false, s);
+  } else {
+    const ModeView v{plane, plane, 0, 1};
+    modal_gemm(A, ld, nl, nl, x, v, y, v, plane, sc, false, s);
+  }
+}
+}  // namespace mfwq

@@ -80,6 +80,9 @@ struct Params {
   const double* x;
   double* y;
   int n1, n2, n3;
+  // slab (multi-GPU) windows, global interior plane indices: x holds planes [v_lo, v_hi),
+  // y holds rows [y_lo, y_hi); the coefficient grids hold quadrature planes from qzb on
+  int v_lo, v_hi, y_lo, y_hi, qzb;
 };
 
 struct Maps {
@@ -330,12 +333,12 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   // v-plane window -> sV[z] (cp.async, zero fill outside the domain); caller commits
   auto fetch_plane = [&](int i3, int z) {
     if (MFWQ_ABLATE == 5) return;
-    const bool vp = i3 >= 0 && i3 < n3;
+    const bool vp = i3 >= prm.v_lo && i3 < prm.v_hi;
     double* dst = sV + z * PV * PV;
     for (int r = warp; r < Dy; r += NWARP) {
       const int g2 = day + r;
       const bool rok = vp && g2 >= 0 && g2 < n2;
-      const double* row = xv + ((size_t)(vp ? i3 : 0) * n2 + (rok ? g2 : 0)) * n1;
+      const double* row = xv + ((size_t)(vp ? i3 - prm.v_lo : 0) * n2 + (rok ? g2 : 0)) * n1;
       for (int c = lane; c < Dx; c += 32) {
         const int g1 = dax + c;
         const bool ok = rok && g1 >= 0 && g1 < n1;
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl)
             tma_load_3d(sC + stage * L::CST + ((ez * 2 + pl) * G + sl) * 256, &maps.m[var][g], tx.q0, ty.q0,
-                        qa + pl, &mbar[stage]);
+                        qa + pl - prm.qzb, &mbar[stage]);
         }
       }
     }
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #pragma unroll
       for (int k = A - ne; k < A; ++k) acc[t][k] = 0.0;
     }
-    if (i3s + ne - 1 < 0 || i3s >= n3) return;  // no valid row (CTA-uniform)
+    if (i3s + ne - 1 < prm.y_lo || i3s >= prm.y_hi) return;  // no valid row (CTA-uniform)
     __syncthreads();
     PROF(6)
 #if MFWQ_ABLATE == 1
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     for (int task = warp; task < ne * NTD * NTD; task += NWARP) {
       const int z = task / (NTD * NTD), mt = (task / NTD) % NTD, nt = task % NTD;
       const int i3 = i3s + z;
-      if (i3 < 0 || i3 >= n3) continue;
+      if (i3 < prm.y_lo || i3 >= prm.y_hi) continue;
       double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
       int chain = 0;
 #pragma unroll
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       d1 += e1;
       const int r = mt * 8 + (lane >> 2), c = nt * 8 + 2 * (lane & 3);
       const int g2 = day + r, g1 = dax + c;
-      const size_t plane = (size_t)i3 * n2;
+      const size_t plane = (size_t)(i3 - prm.y_lo) * n2;
       if (r < Dy && g2 >= 0 && g2 < n2) {
 #if MFWQ_ABLATE == 4  // timing experiment only: plain stores instead of atomics
         if (c < Dx && g1 >= 0 && g1 < n1) yv[(plane + g2) * n1 + g1] = d0;
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     for (int g = 0; g < 6; ++g) {
       if (!grid_used<NT>(g)) { cg[g] = 0.0; continue; }
       if constexpr (kTMA) cg[g] = cst[grid_slot<NT>(g) * 256];
-      else cg[g] = __ldg(prm.C + g * prm.gstride + ((size_t)qz * m2 + ty.q0 + ql2) * prm.m1p + tx.q0 + ql1);
+      else cg[g] = __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * m2 + ty.q0 + ql2) * prm.m1p + tx.q0 + ql1);
     }
     double tv[NT];
 #pragma unroll
@@ -732,11 +735,11 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
         if (tt.nq > f2::TQ || (tt.var == 0 && tt.nq != 2 * (tt.eb - tt.ea))) ok = false;
     } else {
       const long long inplane = (long long)F->ntile[0] * F->ntile[1];
-      int chunk = int(std::max<long long>(4, (long long)S.dir[2].n_el * inplane / (148 * 4) + 1));
+      int chunk = int(std::max<long long>(4, (long long)(S.e_hi - S.e_lo) * inplane / (148 * 4) + 1));
       chunk = std::min(chunk, 64);
       chunk += chunk & 1;  // even chunks: steps of two z-elements
-      for (int e = 0; e < S.dir[2].n_el; e += chunk) {
-        const int b = std::min(S.dir[2].n_el, e + chunk);
+      for (int e = S.e_lo; e < S.e_hi; e += chunk) {
+        const int b = std::min(S.e_hi, e + chunk);
         t.push_back({e, b, S.dir[2].elem_q0[e], S.dir[2].elem_q0[b] - S.dir[2].elem_q0[e], 0});
         F->max_nqz = std::max(F->max_nqz, t.back().nq);
         F->max_chunk = std::max(F->max_chunk, b - e);
@@ -771,7 +774,7 @@ static void encode_maps(Stiffness& S, Fused2Plan& F) {
   const size_t G = S.grid_elems();
   for (int v = 0; v < 4; ++v)
     for (int g = 0; g < 6; ++g) {
-      cuuint64_t dims[3] = {(cuuint64_t)S.dir[0].m, (cuuint64_t)S.dir[1].m, (cuuint64_t)S.dir[2].m};
+      cuuint64_t dims[3] = {(cuuint64_t)S.dir[0].m, (cuuint64_t)S.dir[1].m, (cuuint64_t)(S.q_hi - S.q_lo)};
       cuuint64_t strides[2] = {(cuuint64_t)S.m1p * 8, (cuuint64_t)S.m1p * S.dir[1].m * 8};
       cuuint32_t box[3] = {(cuuint32_t)((v & 1) ? F.bwn : 16), (cuuint32_t)((v & 2) ? F.bwn : 16), 1};
       cuuint32_t es[3] = {1, 1, 1};
@@ -808,6 +811,11 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   prm.m1p = S.m1p;
   prm.x = x;
   prm.y = y;
+  prm.v_lo = S.v_lo;
+  prm.v_hi = S.v_hi;
+  prm.y_lo = S.y_lo;
+  prm.y_hi = S.y_hi;
+  prm.qzb = S.q_lo;
   prm.n1 = S.dir[0].n;
   prm.n2 = S.dir[1].n;
   prm.n3 = S.dir[2].n;
@@ -815,7 +823,7 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   const size_t smem = Smem<P, NT, ZS>::bytes(F.qe, F.max_chunk);
   auto kern = k_fused<P, NT, ZS>;
   MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  MFWQ_CUDA(cudaMemsetAsync(y, 0, S.N * sizeof(double), s));
+  MFWQ_CUDA(cudaMemsetAsync(y, 0, S.out_elems() * sizeof(double), s));
   dim3 grid(F.ntile[0] * F.ntile[1], F.ntile[2]);
   kern<<<grid, NTHR, smem, s>>>(prm, F.maps); note_launch();
   MFWQ_CUDA(cudaGetLastError());

@@ -455,6 +455,7 @@ bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s);
 
 void Stiffness::apply_fused(const double* x, double* y, cudaStream_t s) {
   if (path != 3 && fused2_apply(*this, x, y, s)) return;
+  if (is_slab()) throw NotImplErr("slab operators need the element-blocked fused kernel (p <= 10, n_el >= 2)");
   FusedPlan* F = plan_for(*this);
   if (!F->ok) {  // rule outside the element-blocked structure: composed K1 path (still GPU)
     apply_generic(x, y, s);

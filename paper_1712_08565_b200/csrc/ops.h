@@ -44,6 +44,14 @@ class Stiffness {
   std::shared_ptr<void> fused_plan, fused2_plan;  // element-blocked tables + tiles of the fused kernel
   long long nnz_[3][6] = {};      // interior-restricted nnz per direction: B0,B1,W00,W01,W10,W11
 
+  // slab (multi-GPU) window, global indices: local z-elements [e_lo, e_hi), input planes
+  // [v_lo, v_hi), output rows [y_lo, y_hi), local quadrature planes [q_lo, q_hi)
+  int e_lo = 0, e_hi = 0, v_lo = 0, v_hi = 0, y_lo = 0, y_hi = 0, q_lo = 0, q_hi = 0;
+  bool is_slab() const { return e_lo != 0 || e_hi != dir[2].n_el; }
+  void set_slab(int elo, int ehi);
+  size_t in_elems() const { return size_t(v_hi - v_lo) * dir[0].n * dir[1].n; }
+  size_t out_elems() const { return size_t(y_hi - y_lo) * dir[0].n * dir[1].n; }
+
   // generic-path scratch
   DevBuf<double> g_, t_, s1_, s2_;
   DevBuf<int> flag_;
@@ -59,7 +67,7 @@ class Stiffness {
   void apply(const double* x, double* y, cudaStream_t s);
   void apply_generic(const double* x, double* y, cudaStream_t s);
   void apply_fused(const double* x, double* y, cudaStream_t s);
-  size_t grid_elems() const { return size_t(dir[2].m) * dir[1].m * m1p; }
+  size_t grid_elems() const { return size_t(q_hi - q_lo) * dir[1].m * m1p; }
   int term_mask() const;
   long long flops_for(int mask) const;
  private:
@@ -78,6 +86,9 @@ class FastDiag {
   DevBuf<double> s1_, s2_;
   void init(const int* n, const double* const* K, const double* const* M, double sigma);
   void apply(const double* r, double* z, cudaStream_t s);
+  // one direction of the transform on a local (nz, ny, n1) block (multi-GPU building block)
+  void apply_dir(int dir, int inverse, int scale, const double* x, double* y, int nz, int ny, int row_lo,
+                 cudaStream_t s);
 };
 
 struct KrylovOut {

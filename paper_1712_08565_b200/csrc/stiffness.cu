@@ -102,6 +102,7 @@ void Stiffness::init(const int* p, const int* nknots, const double* const* knots
   N = (long long)dir[0].n * dir[1].n * dir[2].n;
   Nq = (long long)dir[0].m * dir[1].m * dir[2].m;
   m1p = (dir[0].m + 3) / 4 * 4;
+  set_slab(0, dir[2].n_el);
   compute_flops();
   analyse_stencil();
 }
@@ -132,6 +133,25 @@ long long Stiffness::flops_for(int mask) const {
 }
 
 void Stiffness::compute_flops() { flops = flops_for(0x1FF); }
+
+// Slab of z-elements [elo, ehi): element e touches interior DoF planes
+// e-1 .. e+p-1 on the B side and rows e-2 .. e+p-1 on the W side (the breakpoint at
+// the start of e closes the support of full function e-1).
+void Stiffness::set_slab(int elo, int ehi) {
+  const Dir1D& z = dir[2];
+  if (elo < 0 || ehi > z.n_el || elo >= ehi) throw ValueErr("invalid slab element range");
+  e_lo = elo;
+  e_hi = ehi;
+  v_lo = std::max(elo - 1, 0);
+  v_hi = std::min(ehi + z.p - 1, z.n);
+  y_lo = std::max(elo - 2, 0);
+  y_hi = std::min(ehi + z.p - 1, z.n);
+  q_lo = z.elem_q0[elo];
+  q_hi = z.elem_q0[ehi];
+  fused_plan.reset();
+  fused2_plan.reset();
+  coeffs_ready = false;
+}
 
 // ---------------------------------------------------------------------------
 // K5: coefficient grids (operators.py:64-84, geometry.py:47-96)
@@ -239,9 +259,10 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
   double a[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, k[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   if (A) std::copy(A, A + 9, a);
   if (K9) std::copy(K9, K9 + 9, k);
-  const int m1 = dir[0].m, m2 = dir[1].m, m3 = dir[2].m;
-  int blocks = std::min<long long>((Nq + 255) / 256, 148LL * 16);
-  coeff_kernel<<<blocks, 256, 0, s>>>(kind, dir[0].pts_d.ptr, dir[1].pts_d.ptr, dir[2].pts_d.ptr, m1, m2, m3, m1p,
+  const int m1 = dir[0].m, m2 = dir[1].m, m3 = q_hi - q_lo;  // local quadrature planes
+  const long long nql = (long long)m1 * m2 * m3;
+  int blocks = std::min<long long>((nql + 255) / 256, 148LL * 16);
+  coeff_kernel<<<blocks, 256, 0, s>>>(kind, dir[0].pts_d.ptr, dir[1].pts_d.ptr, dir[2].pts_d.ptr + q_lo, m1, m2, m3, m1p,
                                       a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], K9 ? 1 : 0, k[0], k[1],
                                       k[2], k[3], k[4], k[5], k[6], k[7], k[8], J_dev, Kfield_dev, coeff.ptr, G,
                                       bad.ptr); note_launch();
@@ -258,7 +279,7 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
     int q1 = int(q % m1), q2 = int((q / m1) % m2), q3 = int(q / ((long long)m1 * m2));
     char msg[256];
     snprintf(msg, sizeof msg, "non-positive Jacobian determinant at parametric point (%.17g, %.17g, %.17g)",
-             dir[0].pts[q1], dir[1].pts[q2], dir[2].pts[q3]);
+             dir[0].pts[q1], dir[1].pts[q2], dir[2].pts[q_lo + q3]);
     throw DegenerateErr(msg);
   }
   coeffs_ready = true;
@@ -271,9 +292,10 @@ void Stiffness::set_coeffs(const double* const* grids, cudaStream_t s) {
   coeff.alloc(6 * G);
   MFWQ_CUDA(cudaMemsetAsync(coeff.ptr, 0, 6 * G * sizeof(double), s));
   const int m1 = dir[0].m;
-  for (int g = 0; g < 6; ++g)
-    MFWQ_CUDA(cudaMemcpy2DAsync(coeff.ptr + g * G, m1p * sizeof(double), grids[g], m1 * sizeof(double),
-                                m1 * sizeof(double), (size_t)dir[1].m * dir[2].m, cudaMemcpyDeviceToDevice, s));
+  for (int g = 0; g < 6; ++g)  // the slab's quadrature planes of the full (m3, m2, m1) grids
+    MFWQ_CUDA(cudaMemcpy2DAsync(coeff.ptr + g * G, m1p * sizeof(double),
+                                grids[g] + (size_t)q_lo * dir[1].m * m1, m1 * sizeof(double), m1 * sizeof(double),
+                                (size_t)dir[1].m * (q_hi - q_lo), cudaMemcpyDeviceToDevice, s));
   coeffs_ready = true;
   detect_nonzero(s);
 }
@@ -282,7 +304,7 @@ void Stiffness::get_coeffs(int g, double* out, cudaStream_t s) const {
   const size_t G = grid_elems();
   const int m1 = dir[0].m;
   MFWQ_CUDA(cudaMemcpy2DAsync(out, m1 * sizeof(double), coeff.ptr + g * G, m1p * sizeof(double),
-                              m1 * sizeof(double), (size_t)dir[1].m * dir[2].m, cudaMemcpyDeviceToDevice, s));
+                              m1 * sizeof(double), (size_t)dir[1].m * (q_hi - q_lo), cudaMemcpyDeviceToDevice, s));
 }
 
 void Stiffness::detect_nonzero(cudaStream_t s) {
@@ -362,6 +384,7 @@ static void contract(const double* in, double* out, int d1, int d2, int d3, int 
 }
 
 void Stiffness::apply_generic(const double* x, double* y, cudaStream_t s) {
+  if (is_slab()) throw NotImplErr("slab operators run on the fused kernel only");
   const int n1 = dir[0].n, n2 = dir[1].n, n3 = dir[2].n;
   const int m1 = dir[0].m, m2 = dir[1].m, m3 = dir[2].m;
   if (!g_.ptr) {

@@ -33,7 +33,7 @@ def _csr(A):
 class StiffnessOperator:
     """Matrix-free weighted-quadrature stiffness operator (interior space)."""
 
-    def __init__(self, space, rule, geom, K=None, on_the_fly=False):
+    def __init__(self, space, rule, geom, K=None, on_the_fly=False, _slab=None):
         if on_the_fly:
             raise NotImplementedError("on-the-fly coefficient mode is not built yet (SURVEY 8(f) rank 1)")
         _dev.require_cuda()
@@ -74,6 +74,18 @@ class StiffnessOperator:
         self.n, self.m, self.n_points = tuple(int(v) for v in n3), tuple(int(v) for v in m3), Nq.value
         if N.value != self.n_dofs:
             raise ValueError("rule and space disagree on the number of DoFs")
+        # multi-GPU slab of z-elements (paper_1712_08565_b200.dist); None = whole domain
+        self.slab = None
+        self._in_len = self._out_len = self.n_dofs
+        if _slab is not None:
+            _lib.check(L.mfwq_stiffness_set_slab(h, int(_slab[0]), int(_slab[1])))
+            info = np.zeros(6, np.int32)
+            _lib.check(L.mfwq_stiffness_slab_info(h, _lib.iptr(info)))
+            self.slab = dict(e_lo=int(info[0]), e_hi=int(info[1]), v_lo=int(info[2]), v_hi=int(info[3]),
+                             y_lo=int(info[4]), y_hi=int(info[5]))
+            plane = self.n[0] * self.n[1]
+            self._in_len = (self.slab["v_hi"] - self.slab["v_lo"]) * plane
+            self._out_len = (self.slab["y_hi"] - self.slab["y_lo"]) * plane
         self._set_geometry(geom, K)
         fl = C.c_longlong()
         _lib.check(L.mfwq_stiffness_flops(h, C.byref(fl)))
@@ -138,8 +150,8 @@ class StiffnessOperator:
 
     # -- apply (operators.py:185-204) -----------------------------------------
     def apply(self, v, meter: CostMeter | None = None, out=None):
-        x, host = _dev.to_device(v, self.n_dofs)
-        y = out if out is not None else _dev.empty(self.n_dofs)
+        x, host = _dev.to_device(v, self._in_len)
+        y = out if out is not None else _dev.empty(self._out_len)
         _lib.check(_lib.lib().mfwq_stiffness_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
                                                    C.c_void_p(_dev.stream_ptr())))
         if meter is not None:
