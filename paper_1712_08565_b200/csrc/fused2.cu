@@ -83,6 +83,13 @@ struct Params {
   // slab (multi-GPU) windows, global interior plane indices: x holds planes [v_lo, v_hi),
   // y holds rows [y_lo, y_hi); the coefficient grids hold quadrature planes from qzb on
   int v_lo, v_hi, y_lo, y_hi, qzb;
+  // host-prepared operand blocks (see fused2_plan): per x-tile [4][16][PV] Wx^T + [2][16][NB] Bx,
+  // per y-tile [2][16][PKB] By + [4][PV][PK] Wy; element offsets per tile; z table [m3][ZT]
+  const double* xblk;
+  const double* yblk;
+  const int* exy;   // [ntx][16] then [nty][16]
+  const double* ztab;
+  int xblk_sz, yblk_sz;
 };
 
 struct Maps {
@@ -136,6 +143,9 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
@@ -214,7 +224,8 @@ struct Smem {
   static constexpr int oC = 0, oBy = 2 * CST, oWx = oBy + 2 * TQ * PKB, oWy = oWx + NX * TQ * PV,
                        oV = oWy + NY * PV * PK, oAS = oV + ZS * PV * PV, oBx = oAS + AS, oZ = oBx + 2 * TQ * NB;
   static size_t bytes(int qe, int max_chunk) {
-    return sizeof(double) * (size_t)(oZ + 2 * ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + sizeof(int) * (max_chunk + 2);
+    return sizeof(double) * (size_t)(oZ + 2 * ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + sizeof(int) * (max_chunk + 2) +
+           sizeof(int) * ((PV * PV + NTHR - 1) / NTHR) * NTHR;
   }
 };
 
@@ -260,56 +271,33 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   const int bw = tx.var ? prm.bwn : 16, bh = ty.var ? prm.bwn : 16;  // TMA box (x, y)
   const int nez = tz.eb - tz.ea;
 
-  // ---- one-time staging: element offsets, dense band tiles -------------------
-  if (tid < TQ) {
-    sEx[tid] = tid < Tx ? prm.eq[0][tx.q0 + tid] - tx.ea : 0;
-    sEy[tid] = tid < Ty ? prm.eq[1][ty.q0 + tid] - ty.ea : 0;
-  }
-  for (int i = tid; i <= nez; i += NTHR) sQ0[i] = prm.q0z[tz.ea + i];
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-  }
-  for (int i = tid; i < ZS * PV * PV; i += NTHR) sV[i] = 0.0;
-  __syncthreads();
+  // ---- one-time staging: bulk copies of the host-prepared operand blocks --------
   {
-    const double* __restrict__ Bx = prm.B[0];
-    const double* __restrict__ By = prm.B[1];
-    const double* __restrict__ Wx = prm.W[0];
-    const double* __restrict__ Wy = prm.W[1];
-    for (int i = tid; i < 2 * TQ * PKB; i += NTHR) {  // By(q2, r) = Bt[b][q2][r - e(q2) - 1]
-      const int b = i / (TQ * PKB), q = (i / PKB) % TQ, r = i % PKB;
-      const int k = r - sEy[q] - 1;
-      sBy[i] = (q < Ty && k >= 0 && k < NB) ? By[((size_t)b * m2 + ty.q0 + q) * NB + k] : 0.0;
-    }
-    for (int w = 0; w < 4; ++w) {
-      bool xu = false, yu = false;
-      int xs = 0, ys = 0;
+    const double* xb = prm.xblk + (size_t)bxi * prm.xblk_sz;
+    const double* yb = prm.yblk + (size_t)byi * prm.yblk_sz;
+    auto copy16 = [&](double* dst, const double* src, int n) {  // n doubles, even
+      for (int i = 2 * tid; i < n; i += 2 * NTHR) cp_async16(dst + i, src + i);
+    };
+    copy16(sBy, yb, 2 * TQ * PKB);
 #pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (v == w) {
-          xu = xslot<NT>(v + 1) > xslot<NT>(v);  // x-type v used by some term
-          yu = ytype_used<NT>(v);
-          xs = xslot<NT>(v);
-          ys = yslot<NT>(v);
-        }
-      if (xu)
-        for (int i = tid; i < TQ * PV; i += NTHR) {  // Wx^T(ql, c) = Wt[w][ql][c - e(ql)]
-          const int q = i / PV, c = i % PV, k = c - sEx[q];
-          sWxT[xs * TQ * PV + i] = (q < Tx && k >= 0 && k < NW) ? Wx[((size_t)w * m1 + tx.q0 + q) * NW + k] : 0.0;
-        }
-      if (yu)
-        for (int i = tid; i < PV * PK; i += NTHR) {  // Wy(r, q2) = Wt[w][q2][r - e(q2)]
-          const int r = i / PK, q = i % PK;
-          const int k = q < TQ ? r - sEy[q] : -1;
-          sWy[ys * PV * PK + i] = (q < Ty && k >= 0 && k < NW) ? Wy[((size_t)w * m2 + ty.q0 + q) * NW + k] : 0.0;
-        }
+    for (int w = 0; w < 4; ++w) {
+      if (xslot<NT>(w + 1) > xslot<NT>(w)) copy16(sWxT + xslot<NT>(w) * TQ * PV, xb + w * TQ * PV, TQ * PV);
+      if (ytype_used<NT>(w)) copy16(sWy + yslot<NT>(w) * PV * PK, yb + 2 * TQ * PKB + w * PV * PK, PV * PK);
     }
-    for (int i = tid; i < 2 * TQ * NB; i += NTHR) {
-      const int b = i / (TQ * NB), q = (i / NB) % TQ, k = i % NB;
-      sBx[i] = q < Tx ? Bx[((size_t)b * m1 + tx.q0 + q) * NB + k] : 0.0;
+    copy16(sBx, xb + 4 * TQ * PV, 2 * TQ * NB);
+    cp_commit();
+    if (tid < TQ) {
+      sEx[tid] = prm.exy[bxi * TQ + tid];
+      sEy[tid] = prm.exy[(prm.ntx + byi) * TQ + tid];
     }
+    for (int i = tid; i <= nez; i += NTHR) sQ0[i] = prm.q0z[tz.ea + i];
+    if (tid == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    for (int i = tid; i < ZS * PV * PV; i += NTHR) sV[i] = 0.0;
+    cp_wait_all();
   }
   __syncthreads();
 
@@ -327,49 +315,37 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 
   const double* __restrict__ xv = prm.x;
   double* __restrict__ yv = prm.y;
-  const double* __restrict__ ZB = prm.B[2];
-  const double* __restrict__ ZW = prm.W[2];
 
-  // v-plane window -> sV[z] (cp.async, zero fill outside the domain); caller commits
+  // v-plane window -> sV[z] (cp.async, zero fill outside the domain); caller commits.
+  // Each thread owns fixed window cells: their in-plane offsets are computed once.
+  constexpr int FPT = (PV * PV + NTHR - 1) / NTHR;
+  int* sFP = sQ0 + (nez + 2);  // [FPT][NTHR] packed (global in-plane offset << 10 | window cell), -1 = zero
+  for (int k = 0; k < FPT; ++k) {
+    const int e = tid + k * NTHR, r = e / Dx, c = e % Dx, g2 = day + r, g1 = dax + c;
+    const bool inwin = e < Dy * Dx, ok = inwin && g2 >= 0 && g2 < n2 && g1 >= 0 && g1 < n1;
+    sFP[k * NTHR + tid] = !inwin ? -2 : (ok ? ((g2 * n1 + g1) << 10) | (r * PV + c) : -1 - (((r * PV + c)) << 1));
+  }
+  const size_t plane_sz = (size_t)n2 * n1;
   auto fetch_plane = [&](int i3, int z) {
     if (MFWQ_ABLATE == 5) return;
     const bool vp = i3 >= prm.v_lo && i3 < prm.v_hi;
     double* dst = sV + z * PV * PV;
-    for (int r = warp; r < Dy; r += NWARP) {
-      const int g2 = day + r;
-      const bool rok = vp && g2 >= 0 && g2 < n2;
-      const double* row = xv + ((size_t)(vp ? i3 - prm.v_lo : 0) * n2 + (rok ? g2 : 0)) * n1;
-      for (int c = lane; c < Dx; c += 32) {
-        const int g1 = dax + c;
-        const bool ok = rok && g1 >= 0 && g1 < n1;
-        cp_async8(dst + r * PV + c, ok ? row + g1 : xv, ok);
-      }
+    const double* src = xv + (vp ? (size_t)(i3 - prm.v_lo) * plane_sz : 0);
+#pragma unroll
+    for (int k = 0; k < FPT; ++k) {
+      const int code = sFP[k * NTHR + tid];
+      if (code == -2) continue;
+      if (code >= 0) cp_async8(dst + (code & 1023), src + (code >> 10), vp);
+      else cp_async8(dst + ((-1 - code) >> 1), xv, false);  // outside the domain: zero
     }
   };
-  // z tables of chunk elements [el, el+ZS) -> sZ[stage] (plane rows ez*QE + zl)
-  auto fetch_ztab = [&](int el, int stage) {
+  // z tables of chunk elements [el, el+nz): one contiguous block of the flat [m3][ZT] table
+  auto fetch_ztab = [&](int el, int nz, int stage) {
     if (MFWQ_ABLATE == 6) return;
     double* dst = sZ + stage * ZS * QE * ZT;
-#pragma unroll
-    for (int ez = 0; ez < ZS; ++ez) {
-      if (el + ez >= nez) break;
-      const int qa = sQ0[el + ez], nq = sQ0[el + ez + 1] - qa;
-      for (int i = tid; i < nq * ZT; i += NTHR) {
-        const int zl = i / ZT, j = i % ZT;
-        const double* src;
-        bool ok = true;
-        if (j < 2 * NBP) {
-          const int b = j / NBP, k = j % NBP;
-          ok = k < NB;
-          src = ZB + ((size_t)b * m3 + qa + zl) * NB + (ok ? k : 0);
-        } else {
-          const int w = (j - 2 * NBP) / NWP, k = (j - 2 * NBP) % NWP;
-          ok = k < NW;
-          src = ZW + ((size_t)w * m3 + qa + zl) * NW + (ok ? k : 0);
-        }
-        cp_async8(dst + (ez * QE + zl) * ZT + j, src, ok);
-      }
-    }
+    const int qa = sQ0[el], n = (sQ0[el + nz] - qa) * ZT;
+    const double* src = prm.ztab + (size_t)qa * ZT;
+    for (int i = 2 * tid; i < n; i += 2 * NTHR) cp_async16(dst + i, src + i);
   };
   // coefficient planes of chunk elements [el, el+ZS) (2 planes each) -> sC[stage] by TMA
   auto issue_coeff = [&](int el, int stage) {
@@ -611,7 +587,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   {
     const int nz0 = nez >= ZS ? ZS : 1;
     for (int z = 0; z < nz0; ++z) fetch_plane(tz.ea + P - 1 + z, z);
-    fetch_ztab(0, 0);
+    fetch_ztab(0, nez >= ZS ? ZS : 1, 0);
     cp_commit();
     if (step_tma(0)) issue_coeff(0, 0);
   }
@@ -627,7 +603,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     const int eln = el + nz;
     const int nzn = (nez - eln) >= ZS ? ZS : 1;
     if (eln < nez) {
-      fetch_ztab(eln, s ^ 1);
+      fetch_ztab(eln, nzn, s ^ 1);
       if (step_tma(eln)) issue_coeff(eln, s ^ 1);
     }
     PROF(1)
@@ -651,13 +627,14 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       for (int ez = 0; ez < nz; ++ez)
 #pragma unroll
         for (int pl = 0; pl < 2; ++pl)
-          zpoint(std::true_type{}, 0, ro0 + ez, ez, zt + (ez * QE + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
+          zpoint(std::true_type{}, 0, ro0 + ez, ez, zt + (sQ0[el + ez] - sQ0[el] + pl) * ZT,
+                 cst + (ez * 2 + pl) * G * 256);
     } else {  // boundary z-elements (extra planes) or the odd tail: C straight from global
 #pragma unroll
       for (int ez = 0; ez < nz; ++ez) {
         const int qa = sQ0[el + ez], nq = sQ0[el + ez + 1] - qa;
         for (int zl = 0; zl < nq; ++zl)
-          zpoint(std::false_type{}, qa + zl, ro0 + ez, ez, zt + (ez * QE + zl) * ZT, nullptr);
+          zpoint(std::false_type{}, qa + zl, ro0 + ez, ez, zt + (qa - sQ0[el] + zl) * ZT, nullptr);
       }
     }
     PROF(5)
@@ -685,7 +662,9 @@ struct Fused2Plan {
   bool ok = false;
   int p = 0, bwn = 0;
   DevBuf<double> B[3], W[3];
-  DevBuf<int> eq[3], q0z;
+  DevBuf<int> eq[3], q0z, exy;
+  DevBuf<double> xblk, yblk, ztab;  // host-prepared per-tile operand blocks, flat z table
+  int xblk_sz = 0, yblk_sz = 0;
   DevBuf<f2::Tile> tiles[3];
   int ntile[3] = {0, 0, 0};
   int max_nqz = 0, qe = 0, max_chunk = 0;
@@ -719,24 +698,31 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
   bool ok = p >= 1 && p <= 10 && S.dir[1].p == p && S.dir[2].p == p;
   for (int l = 0; l < 3 && ok; ++l) ok = S.dir[l].n_el >= 2;
   int maxe = 0;
+  std::vector<double> HB[3], HW[3];
+  std::vector<int> Heq[3];
+  std::vector<f2::Tile> T[3];
   for (int l = 0; l < 3 && ok; ++l) {
-    std::vector<double> B, W;
-    std::vector<int> eq;
+    std::vector<double>& B = HB[l];
+    std::vector<double>& W = HW[l];
+    std::vector<int>& eq = Heq[l];
     ok = build_elem_tables(S.dir[l], B, W, eq);
     if (!ok) break;
     F->B[l].upload(B.data(), B.size());
     F->W[l].upload(W.data(), W.size());
     F->eq[l].upload(eq.data(), eq.size());
     for (int e = 0; e < S.dir[l].n_el; ++e) maxe = std::max(maxe, S.dir[l].elem_q0[e + 1] - S.dir[l].elem_q0[e]);
-    std::vector<f2::Tile> t;
+    std::vector<f2::Tile>& t = T[l];
     if (l < 2) {
       t = f2_tiles_inplane(S.dir[l]);
       for (auto& tt : t)
         if (tt.nq > f2::TQ || (tt.var == 0 && tt.nq != 2 * (tt.eb - tt.ea))) ok = false;
     } else {
       const long long inplane = (long long)F->ntile[0] * F->ntile[1];
-      int chunk = int(std::max<long long>(4, (long long)(S.e_hi - S.e_lo) * inplane / (148 * 4) + 1));
+      // z-chunk length: as long as possible (the ring prologue costs p planes per chunk) while
+      // keeping >= ~4 waves of 2 CTAs x 148 SMs so the last wave's tail stays small
+      int chunk = int(std::max<long long>(8, (long long)(S.e_hi - S.e_lo) * inplane / (4 * 2 * 148)));
       chunk = std::min(chunk, 64);
+      if (const char* ev = getenv("MFWQ_CHUNK")) chunk = std::max(2, atoi(ev));  // tuning experiments
       chunk += chunk & 1;  // even chunks: steps of two z-elements
       for (int e = S.e_lo; e < S.e_hi; e += chunk) {
         const int b = std::min(S.e_hi, e + chunk);
@@ -748,6 +734,59 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
     }
     F->ntile[l] = int(t.size());
     F->tiles[l].upload(t.data(), t.size());
+  }
+  if (ok) {  // dense per-tile operand blocks (the band matrices of one tile, zero padded)
+    using namespace f2;
+    const int NB = p + 1, NW = p + 2, NBP = (NB + 1) & ~1, NWP = (NW + 1) & ~1, ZT = 2 * NBP + 4 * NWP;
+    const int m1 = S.dir[0].m, m2 = S.dir[1].m, m3 = S.dir[2].m;
+    F->xblk_sz = 4 * TQ * PV + 2 * TQ * NB;
+    F->yblk_sz = 2 * TQ * PKB + 4 * PV * PK;
+    std::vector<double> xb((size_t)F->ntile[0] * F->xblk_sz, 0.0), yb((size_t)F->ntile[1] * F->yblk_sz, 0.0);
+    std::vector<int> exy((size_t)(F->ntile[0] + F->ntile[1]) * TQ, 0);
+    for (int i = 0; i < F->ntile[0]; ++i) {
+      const Tile& t = T[0][i];
+      double* o = xb.data() + (size_t)i * F->xblk_sz;
+      for (int q = 0; q < t.nq; ++q) {
+        const int ex = Heq[0][t.q0 + q] - t.ea;
+        exy[i * TQ + q] = ex;
+        for (int w = 0; w < 4; ++w)  // Wx^T(ql, c) = Wt[w][ql][c - e(ql)]
+          for (int c = 0; c < PV; ++c) {
+            const int k = c - ex;
+            if (k >= 0 && k < NW) o[(w * TQ + q) * PV + c] = HW[0][((size_t)w * m1 + t.q0 + q) * NW + k];
+          }
+        for (int b = 0; b < 2; ++b)
+          for (int k = 0; k < NB; ++k) o[4 * TQ * PV + (b * TQ + q) * NB + k] = HB[0][((size_t)b * m1 + t.q0 + q) * NB + k];
+      }
+    }
+    for (int i = 0; i < F->ntile[1]; ++i) {
+      const Tile& t = T[1][i];
+      double* o = yb.data() + (size_t)i * F->yblk_sz;
+      for (int q = 0; q < t.nq; ++q) {
+        const int ey = Heq[1][t.q0 + q] - t.ea;
+        exy[(F->ntile[0] + i) * TQ + q] = ey;
+        for (int b = 0; b < 2; ++b)  // By(q2, r) = Bt[b][q2][r - e(q2) - 1]
+          for (int r = 0; r < PKB; ++r) {
+            const int k = r - ey - 1;
+            if (k >= 0 && k < NB) o[(b * TQ + q) * PKB + r] = HB[1][((size_t)b * m2 + t.q0 + q) * NB + k];
+          }
+        for (int w = 0; w < 4; ++w)  // Wy(r, q2) = Wt[w][q2][r - e(q2)]
+          for (int r = 0; r < PV; ++r) {
+            const int k = r - ey;
+            if (k >= 0 && k < NW) o[2 * TQ * PKB + (w * PV + r) * PK + q] = HW[1][((size_t)w * m2 + t.q0 + q) * NW + k];
+          }
+      }
+    }
+    std::vector<double> zt((size_t)m3 * ZT, 0.0);  // z rows: B0 | B1 | W00 W01 W10 W11, sub-tables padded to even
+    for (int q = 0; q < m3; ++q) {
+      for (int b = 0; b < 2; ++b)
+        for (int k = 0; k < NB; ++k) zt[(size_t)q * ZT + b * NBP + k] = HB[2][((size_t)b * m3 + q) * NB + k];
+      for (int w = 0; w < 4; ++w)
+        for (int k = 0; k < NW; ++k) zt[(size_t)q * ZT + 2 * NBP + w * NWP + k] = HW[2][((size_t)w * m3 + q) * NW + k];
+    }
+    F->xblk.upload(xb.data(), xb.size());
+    F->yblk.upload(yb.data(), yb.size());
+    F->exy.upload(exy.data(), exy.size());
+    F->ztab.upload(zt.data(), zt.size());
   }
   F->bwn = (maxe + 1) / 2 * 2;
   F->qe = maxe;
@@ -811,6 +850,12 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   prm.m1p = S.m1p;
   prm.x = x;
   prm.y = y;
+  prm.xblk = F.xblk.ptr;
+  prm.yblk = F.yblk.ptr;
+  prm.exy = F.exy.ptr;
+  prm.ztab = F.ztab.ptr;
+  prm.xblk_sz = F.xblk_sz;
+  prm.yblk_sz = F.yblk_sz;
   prm.v_lo = S.v_lo;
   prm.v_hi = S.v_hi;
   prm.y_lo = S.y_lo;

@@ -1,0 +1,30 @@
+"""Aggregate ncu SASS samples/instructions by source-line ranges (phases).
+    python tools/ncu_phases.py report obj kernel_substring name:lo-hi [name:lo-hi ...]"""
+import subprocess, sys, os, re, csv, io, tempfile
+rep, obj, ks = sys.argv[1], os.path.abspath(sys.argv[2]), sys.argv[3]
+ranges = []
+for a in sys.argv[4:]:
+    n, r = a.split(':'); lo, hi = r.split('-'); ranges.append((n, int(lo), int(hi)))
+src = list(csv.reader(io.StringIO(subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv'], capture_output=True, text=True).stdout)))
+hdr = src[1]; rows = [dict(zip(hdr, x)) for x in src[2:]]
+with tempfile.TemporaryDirectory() as d:
+    subprocess.run(['cuobjdump', '-xelf', 'all', obj], cwd=d, capture_output=True)
+    cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith('.cubin')][0]
+    dis = subprocess.run(['nvdisasm', '-g', '-c', cub], capture_output=True, text=True).stdout
+funcs = re.split(r'\n\s*\.text\.(\S+):', dis)
+body = next(funcs[i + 1] for i in range(1, len(funcs), 2) if ks in funcs[i])
+line, lines = None, []
+for ln in body.split('\n'):
+    m = re.search(r'//## File ".*?", line (\d+)', ln)
+    if m: line = int(m.group(1)); continue
+    if re.match(r'\s*/\*[0-9a-f]{4,}\*/', ln): lines.append(line)
+agg = {}
+ti = sum(int(x['Instructions Executed'] or 0) for x in rows) or 1
+ts = sum(int(x['Warp Stall Sampling (All Samples)'] or 0) for x in rows) or 1
+for x, l in zip(rows, lines):
+    name = 'other'
+    for n, lo, hi in ranges:
+        if l is not None and lo <= l <= hi: name = n; break
+    a = agg.setdefault(name, [0, 0]); a[0] += int(x['Instructions Executed'] or 0); a[1] += int(x['Warp Stall Sampling (All Samples)'] or 0)
+for n, (i, s) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f'{n:12s} inst {100*i/ti:5.1f}%  ({i/1e6:7.1f} M)   samples {100*s/ts:5.1f}%')
