@@ -29,6 +29,9 @@ struct DevBuf {
     n = count;
     if (count) MFWQ_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
   }
+  void alloc_at_least(size_t count) {
+    if (count > n) alloc(count);
+  }
   void upload(const T* host, size_t count, cudaStream_t s = 0) {
     if (count > n) alloc(count);
     if (count) MFWQ_CUDA(cudaMemcpyAsync(ptr, host, count * sizeof(T), cudaMemcpyHostToDevice, s));

@@ -52,6 +52,8 @@ class Stiffness {
   size_t in_elems() const { return size_t(v_hi - v_lo) * dir[0].n * dir[1].n; }
   size_t out_elems() const { return size_t(y_hi - y_lo) * dir[0].n * dir[1].n; }
 
+  DevBuf<double> pcg_ws;  // PCG work vectors (r, z, p, Ap) + reduction partials, reused across solves
+
   // generic-path scratch
   DevBuf<double> g_, t_, s1_, s2_;
   DevBuf<int> flag_;

@@ -86,7 +86,13 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
   hist.clear();
   out = KrylovOut{};
   MFWQ_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s));
-  DevBuf<double> part(RGRID), sc(4);  // sc: 0 rz, 1 pAp, 2 rr, 3 rz_new
+  // persistent workspace on the operator (no cudaMalloc/cudaFree inside the solve)
+  A.pcg_ws.alloc_at_least(4 * N + RGRID + 4);
+  double* r = A.pcg_ws.ptr;
+  double* z = r + N;
+  double* p = z + N;
+  double* Ap = p + N;
+  struct { double* ptr; } part{Ap + N}, sc{Ap + N + RGRID};  // sc: 0 rz, 1 pAp, 2 rr, 3 rz_new
   double* rz = sc.ptr;
   double* pAp = sc.ptr + 1;
   double* rr = sc.ptr + 2;
@@ -101,19 +107,18 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
     out.converged = 1;
     return;
   }
-  DevBuf<double> r(N), z(N), p(N), Ap(N);
-  MFWQ_CUDA(cudaMemcpyAsync(r.ptr, b, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  if (P) P->apply(r.ptr, z.ptr, s);
-  else MFWQ_CUDA(cudaMemcpyAsync(z.ptr, r.ptr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  MFWQ_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (P) P->apply(r, z, s);
+  else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
   out.precs = 1;
-  MFWQ_CUDA(cudaMemcpyAsync(p.ptr, z.ptr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  dot_to(r.ptr, z.ptr, N, part.ptr, rz, s);
+  MFWQ_CUDA(cudaMemcpyAsync(p, z, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  dot_to(r, z, N, part.ptr, rz, s);
   hist.push_back(1.0);
   for (int k = 1; k <= maxit; ++k) {
-    A.apply(p.ptr, Ap.ptr, s);
+    A.apply(p, Ap, s);
     out.matvecs++;
-    dot_to(p.ptr, Ap.ptr, N, part.ptr, pAp, s);
-    update_xr<<<RGRID, RB, 0, s>>>(x, r.ptr, p.ptr, Ap.ptr, N, rz, pAp, part.ptr); note_launch();
+    dot_to(p, Ap, N, part.ptr, pAp, s);
+    update_xr<<<RGRID, RB, 0, s>>>(x, r, p, Ap, N, rz, pAp, part.ptr); note_launch();
     finish_sum<<<1, RB, 0, s>>>(part.ptr, RGRID, rr); note_launch();
     MFWQ_CUDA(cudaGetLastError());
     MFWQ_CUDA(cudaMemcpyAsync(h2, pAp, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -130,11 +135,11 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
       out.converged = 1;
       return;
     }
-    if (P) P->apply(r.ptr, z.ptr, s);
-    else MFWQ_CUDA(cudaMemcpyAsync(z.ptr, r.ptr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (P) P->apply(r, z, s);
+    else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     out.precs++;
-    dot_to(r.ptr, z.ptr, N, part.ptr, rzn, s);
-    update_p<<<RGRID, RB, 0, s>>>(p.ptr, z.ptr, N, rzn, rz); note_launch();
+    dot_to(r, z, N, part.ptr, rzn, s);
+    update_p<<<RGRID, RB, 0, s>>>(p, z, N, rzn, rz); note_launch();
     copy_scalar<<<1, 1, 0, s>>>(rzn, rz); note_launch();
     MFWQ_CUDA(cudaGetLastError());
   }
