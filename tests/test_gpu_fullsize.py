@@ -1,0 +1,30 @@
+"""Parity at the BASELINE cfg-2 size (n_el = 128, p = 2..6) against anchors produced by
+running the reference itself (tests/golden/full_anchors.json, make_golden.py --full)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1712_08565_b200 as M
+
+pytestmark = pytest.mark.gpu
+ANCH = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "full_anchors.json")))
+# the native WQ rule agrees with the reference lstsq to ~1e-13 (p <= 5) / ~1e-11 (p = 6)
+TOL = {2: 1e-12, 3: 1e-12, 4: 1e-12, 5: 1e-12, 6: 1e-10}
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6])
+def test_cfg2_matvec_anchor(p):
+    a = ANCH[f"cfg2_p{p}"]
+    space = M.tensor_space(p, 128)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.identity_map(3))
+    assert space.n_dofs == a["N"]
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(space.n_dofs)).cuda()
+    y = A.apply(x).cpu().numpy()
+    assert abs(np.linalg.norm(y) - a["norm_y"]) <= TOL[p] * a["norm_y"]
+    head, tail = np.array(a["y_head"]), np.array(a["y_tail"])
+    scale = np.abs(y).max()
+    assert np.abs(y[:8] - head).max() <= TOL[p] * 1e2 * scale
+    assert np.abs(y[-8:] - tail).max() <= TOL[p] * 1e2 * scale
