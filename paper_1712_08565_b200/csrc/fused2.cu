@@ -58,7 +58,6 @@ constexpr int PKB = 28;  // pitch of By (K = window rows, up to 24)
 struct Tile {
   int ea, eb;  // elements [ea, eb)
   int q0, nq;  // quadrature points [q0, q0+nq)
-  int var;     // TMA box variant index along this direction (0 = 16 wide, 1 = narrow)
 };
 
 struct Params {
@@ -72,7 +71,6 @@ struct Params {
   int ntx, nty;
   int m[3];
   int nel3;
-  int bwn;             // narrow box width (even)
   int qe;              // max quadrature planes per z-element
   const double* C;     // 6 grids (padded pitch m1p)
   size_t gstride;
@@ -93,7 +91,7 @@ struct Params {
 };
 
 struct Maps {
-  CUtensorMap m[4][6];  // [variant = 2*ynarrow + xnarrow][grid]
+  CUtensorMap m[6];  // per coefficient grid, 16 x 16 x 1 boxes (zero fill past the grid edge)
 };
 
 template <int NT>
@@ -267,8 +265,6 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   const int dax = tx.ea - 2, day = ty.ea - 2;
   const int n1 = prm.n1, n2 = prm.n2, n3 = prm.n3;
   const int m1 = prm.m[0], m2 = prm.m[1], m3 = prm.m[2];
-  const int var = 2 * ty.var + tx.var;
-  const int bw = tx.var ? prm.bwn : 16, bh = ty.var ? prm.bwn : 16;  // TMA box (x, y)
   const int nez = tz.eb - tz.ea;
 
   // ---- one-time staging: bulk copies of the host-prepared operand blocks --------
@@ -350,7 +346,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   // coefficient planes of chunk elements [el, el+ZS) (2 planes each) -> sC[stage] by TMA
   auto issue_coeff = [&](int el, int stage) {
     if (tid == 0) {
-      mbar_expect_tx(&mbar[stage], ZS * G * 2 * bw * bh * 8);
+      mbar_expect_tx(&mbar[stage], ZS * G * 2 * TQ * TQ * 8);
 #pragma unroll
       for (int ez = 0; ez < ZS; ++ez) {
         const int qa = sQ0[el + ez];
@@ -360,7 +356,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
           const int sl = grid_slot<NT>(g);
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl)
-            tma_load_3d(sC + stage * L::CST + ((ez * 2 + pl) * G + sl) * 256, &maps.m[var][g], tx.q0, ty.q0,
+            tma_load_3d(sC + stage * L::CST + ((ez * 2 + pl) * G + sl) * 256, &maps.m[g], tx.q0, ty.q0,
                         qa + pl - prm.qzb, &mbar[stage]);
         }
       }
@@ -570,7 +566,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       }
     }
   };
-  const int cthr = ql2 * bw + ql1;  // this thread's point inside a TMA coefficient box
+  const int cthr = ql2 * TQ + ql1;  // this thread's point inside a TMA coefficient box
 
   // ---- prologue: fill the ring with planes ea-1 .. ea+p-2 ----------------------
   for (int k = 0; k < P; ++k) {
@@ -660,7 +656,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 // ---------------------------------------------------------------------------
 struct Fused2Plan {
   bool ok = false;
-  int p = 0, bwn = 0;
+  int p = 0;
   DevBuf<double> B[3], W[3];
   DevBuf<int> eq[3], q0z, exy;
   DevBuf<double> xblk, yblk, ztab;  // host-prepared per-tile operand blocks, flat z table
@@ -675,18 +671,19 @@ struct Fused2Plan {
 bool build_elem_tables(const Dir1D& d, std::vector<double>& B, std::vector<double>& W, std::vector<int>& eq);
 
 static std::vector<f2::Tile> f2_tiles_inplane(const Dir1D& d) {
+  // greedy element-aligned tiles of <= 16 quadrature points from element 0: with an even
+  // number of boundary extras every tile but the last is exactly 16 points wide, so the
+  // boundary elements ride along with their neighbours instead of forming thin strips
   std::vector<f2::Tile> t;
   const int n = d.n_el;
   auto nq = [&](int a, int b) { return d.elem_q0[b] - d.elem_q0[a]; };
-  auto push = [&](int a, int b, int var) { t.push_back({a, b, d.elem_q0[a], nq(a, b), var}); };
-  push(0, 1, 1);  // first element alone (boundary extras)
-  int e = 1;
-  while (e < n - 1) {
-    int b = std::min(n - 1, e + 8);
-    push(e, b, 0);
+  int e = 0;
+  while (e < n) {
+    int b = e + 1;
+    while (b < n && nq(e, b + 1) <= f2::TQ) ++b;
+    t.push_back({e, b, d.elem_q0[e], nq(e, b)});
     e = b;
   }
-  if (n > 1) push(n - 1, n, 1);
   return t;
 }
 
@@ -715,18 +712,32 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
     if (l < 2) {
       t = f2_tiles_inplane(S.dir[l]);
       for (auto& tt : t)
-        if (tt.nq > f2::TQ || (tt.var == 0 && tt.nq != 2 * (tt.eb - tt.ea))) ok = false;
+        if (tt.nq > f2::TQ) ok = false;
     } else {
+      // z-chunks: minimise waves x (chunk + ring prologue + setup) over the CTA slots of the
+      // occupancy the kernel gets (2 or 1 CTAs per SM)
       const long long inplane = (long long)F->ntile[0] * F->ntile[1];
-      // z-chunk length: as long as possible (the ring prologue costs p planes per chunk) while
-      // keeping >= ~4 waves of 2 CTAs x 148 SMs so the last wave's tail stays small
-      int chunk = int(std::max<long long>(8, (long long)(S.e_hi - S.e_lo) * inplane / (4 * 2 * 148)));
-      chunk = std::min(chunk, 64);
+      const int mask = S.term_mask();
+      const int nt = (mask & ~0x111) == 0 ? 3 : ((mask & ~0x11B) == 0 ? 5 : 9);
+      const int occ = (nt == 3 && p <= 6) || (nt == 5 && p <= 2) ? 2 : 1;
+      int dev = 0, nsm = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const long long slots = (long long)occ * nsm;
+      const int E = S.e_hi - S.e_lo;
+      int chunk = E + (E & 1);
+      double best = 1e300;
+      for (int nch = 1; nch <= std::max(1, E / 4); ++nch) {
+        int len = (E + nch - 1) / nch;
+        len += len & 1;
+        const long long ctas = inplane * ((E + len - 1) / len);
+        const double cost = double((ctas + slots - 1) / slots) * (len + p + 4);
+        if (cost < best - 1e-9) { best = cost; chunk = len; }
+      }
       if (const char* ev = getenv("MFWQ_CHUNK")) chunk = std::max(2, atoi(ev));  // tuning experiments
       chunk += chunk & 1;  // even chunks: steps of two z-elements
       for (int e = S.e_lo; e < S.e_hi; e += chunk) {
         const int b = std::min(S.e_hi, e + chunk);
-        t.push_back({e, b, S.dir[2].elem_q0[e], S.dir[2].elem_q0[b] - S.dir[2].elem_q0[e], 0});
+        t.push_back({e, b, S.dir[2].elem_q0[e], S.dir[2].elem_q0[b] - S.dir[2].elem_q0[e]});
         F->max_nqz = std::max(F->max_nqz, t.back().nq);
         F->max_chunk = std::max(F->max_chunk, b - e);
       }
@@ -788,10 +799,9 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
     F->exy.upload(exy.data(), exy.size());
     F->ztab.upload(zt.data(), zt.size());
   }
-  F->bwn = (maxe + 1) / 2 * 2;
   F->qe = maxe;
   F->p = p;
-  F->ok = ok && F->bwn <= 16;
+  F->ok = ok && maxe <= f2::TQ;
   return F;
 }
 
@@ -811,17 +821,16 @@ static void encode_maps(Stiffness& S, Fused2Plan& F) {
   if (F.maps_for == S.coeff.ptr) return;
   auto enc = get_encode();
   const size_t G = S.grid_elems();
-  for (int v = 0; v < 4; ++v)
-    for (int g = 0; g < 6; ++g) {
-      cuuint64_t dims[3] = {(cuuint64_t)S.dir[0].m, (cuuint64_t)S.dir[1].m, (cuuint64_t)(S.q_hi - S.q_lo)};
-      cuuint64_t strides[2] = {(cuuint64_t)S.m1p * 8, (cuuint64_t)S.m1p * S.dir[1].m * 8};
-      cuuint32_t box[3] = {(cuuint32_t)((v & 1) ? F.bwn : 16), (cuuint32_t)((v & 2) ? F.bwn : 16), 1};
-      cuuint32_t es[3] = {1, 1, 1};
-      CUresult r = enc(&F.maps.m[v][g], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(S.coeff.ptr + g * G), dims,
-                       strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw CudaErr("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-    }
+  for (int g = 0; g < 6; ++g) {
+    cuuint64_t dims[3] = {(cuuint64_t)S.dir[0].m, (cuuint64_t)S.dir[1].m, (cuuint64_t)(S.q_hi - S.q_lo)};
+    cuuint64_t strides[2] = {(cuuint64_t)S.m1p * 8, (cuuint64_t)S.m1p * S.dir[1].m * 8};
+    cuuint32_t box[3] = {(cuuint32_t)f2::TQ, (cuuint32_t)f2::TQ, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&F.maps.m[g], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(S.coeff.ptr + g * G), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaErr("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  }
   F.maps_for = S.coeff.ptr;
 }
 
@@ -844,7 +853,6 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   prm.ntx = F.ntile[0];
   prm.nty = F.ntile[1];
   prm.nel3 = S.dir[2].n_el;
-  prm.bwn = F.bwn;
   prm.C = S.coeff.ptr;
   prm.gstride = S.grid_elems();
   prm.m1p = S.m1p;
