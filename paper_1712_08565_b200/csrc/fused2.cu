@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     k_fused(const __grid_constant__ Params prm, const __grid_constant__ Maps maps) {
   using L = Smem<P, NT, ZS>;
   constexpr int NB = L::NB, NW = L::NW, NBP = L::NBP, NWP = L::NWP, ZT = L::ZT, G = L::G;
-  constexpr int R = NB + ZS - 1;                 // ring slots (B side)
+  constexpr int R = NB;                          // ring slots (B side): pushed right before use
   constexpr int A = NW + ZS - 1;                 // accumulator slots (W side)
   constexpr int DMAX = TQ / 2 + P + 1;           // DoF window bound (8 elements + p + 1)
   constexpr int NTD = (DMAX + 7) / 8;            // 8-wide tiles over a window dimension
@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   const int Tx = tx.nq, Ty = ty.nq;
   const int Dx = tx.eb - tx.ea + P + 1, Dy = ty.eb - ty.ea + P + 1;
   const int dax = tx.ea - 2, day = ty.ea - 2;
-  const int n1 = prm.n1, n2 = prm.n2, n3 = prm.n3;
-  const int m1 = prm.m[0], m2 = prm.m[1], m3 = prm.m[2];
+  const int n1 = prm.n1, n2 = prm.n2;
+  const int m2 = prm.m[1];
   const int nez = tz.eb - tz.ea;
 
   // ---- one-time staging: bulk copies of the host-prepared operand blocks --------
@@ -533,13 +533,15 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         gz = fma(c1.y, h0[ro + k + 1], gz);
       }
     }
-    if (!active || MFWQ_ABLATE == 3) return;
+    if (MFWQ_ABLATE == 3) return;
+    // inactive lanes (outside a narrow tile) run the same code with zero coefficients: no
+    // divergent exit, so the accumulator registers need no reconciling moves
     double cg[6];
 #pragma unroll
     for (int g = 0; g < 6; ++g) {
       if (!grid_used<NT>(g)) { cg[g] = 0.0; continue; }
-      if constexpr (kTMA) cg[g] = cst[grid_slot<NT>(g) * 256];
-      else cg[g] = __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * m2 + ty.q0 + ql2) * prm.m1p + tx.q0 + ql1);
+      if constexpr (kTMA) cg[g] = active ? cst[grid_slot<NT>(g) * 256] : 0.0;
+      else cg[g] = active ? __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * m2 + ty.q0 + ql2) * prm.m1p + tx.q0 + ql1) : 0.0;
     }
     double tv[NT];
 #pragma unroll
@@ -587,7 +589,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     cp_commit();
     if (step_tma(0)) issue_coeff(0, 0);
   }
-  unsigned parity[2] = {0u, 0u};
+  unsigned parity = 0u;  // bit s: phase of mbar[s] (a register, not a local array)
 
   // one step over NZ (compile-time) z-elements starting at chunk element el, stage s
   auto do_step = [&](auto NZc, int el, int s) {
@@ -609,28 +611,26 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     if (eln < nez)
       for (int z = 0; z < nzn; ++z) fetch_plane(e3 + nz + P - 1 + z, z);  // next step's planes
     cp_commit();
-#pragma unroll
-    for (int z = 0; z < nz; ++z) push_x(z);  // ring: planes up to e3+p+nz-2
-    PROF(3)
-    constexpr int ro0 = ZS - nz;  // ring offset of the step's first element
     const double* zt = sZ + s * ZS * QE * ZT;
     if (nz == ZS && step_tma(el)) {
-      mbar_wait(&mbar[s], parity[s]);
-      parity[s] ^= 1u;
+      mbar_wait(&mbar[s], (parity >> s) & 1u);
+      parity ^= 1u << s;
       PROF(4)
       const double* cst = sC + s * L::CST + cthr;
 #pragma unroll
-      for (int ez = 0; ez < nz; ++ez)
+      for (int ez = 0; ez < nz; ++ez) {
+        push_x(ez);  // ring: planes e3+ez-1 .. e3+ez+p-1, exactly the support of element e3+ez
 #pragma unroll
         for (int pl = 0; pl < 2; ++pl)
-          zpoint(std::true_type{}, 0, ro0 + ez, ez, zt + (sQ0[el + ez] - sQ0[el] + pl) * ZT,
-                 cst + (ez * 2 + pl) * G * 256);
+          zpoint(std::true_type{}, 0, 0, ez, zt + (sQ0[el + ez] - sQ0[el] + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
+      }
     } else {  // boundary z-elements (extra planes) or the odd tail: C straight from global
 #pragma unroll
       for (int ez = 0; ez < nz; ++ez) {
+        push_x(ez);
         const int qa = sQ0[el + ez], nq = sQ0[el + ez + 1] - qa;
         for (int zl = 0; zl < nq; ++zl)
-          zpoint(std::false_type{}, qa + zl, ro0 + ez, ez, zt + (qa - sQ0[el] + zl) * ZT, nullptr);
+          zpoint(std::false_type{}, qa + zl, 0, ez, zt + (qa - sQ0[el] + zl) * ZT, nullptr);
       }
     }
     PROF(5)
@@ -893,6 +893,11 @@ static void dispatch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, c
 bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s) {
   Fused2Plan* F = fused2_plan(S);
   if (!F->ok) return false;
+#ifdef MFWQ_ONLY_P  // static-analysis builds of one degree (tools/sass_stats.sh); never in the product
+  if (F->p != MFWQ_ONLY_P) return false;
+  dispatch2<MFWQ_ONLY_P>(S, *F, x, y, s);
+  return true;
+#endif
   switch (F->p) {
     case 1: dispatch2<1>(S, *F, x, y, s); break;
     case 2: dispatch2<2>(S, *F, x, y, s); break;

@@ -16,8 +16,13 @@ hdr = src[1]
 rows = [dict(zip(hdr, x)) for x in src[2:]]
 with tempfile.TemporaryDirectory() as d:
     subprocess.run(['cuobjdump', '-xelf', 'all', obj], cwd=d, capture_output=True)
-    cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith('.cubin')][0]
-    dis = subprocess.run(['nvdisasm', '-g', '-c', cub], capture_output=True, text=True).stdout
+    dis = ''
+    for f in sorted(os.listdir(d)):  # the cubin that holds the kernel
+        if f.endswith('.cubin'):
+            t = subprocess.run(['nvdisasm', '-g', '-c', os.path.join(d, f)], capture_output=True, text=True).stdout
+            if ksub in t:
+                dis = t
+                break
 # split per function
 funcs = re.split(r'\n\s*\.text\.(\S+):', dis)
 body = None
@@ -28,9 +33,9 @@ for i in range(1, len(funcs), 2):
 line = None
 lines = []
 for ln in body.split('\n'):
-    m = re.search(r'//## File ".*?", line (\d+)', ln)
+    m = re.search(r'//## File "(.*?)", line (\d+)', ln)
     if m:
-        line = int(m.group(1))
+        line = (os.path.basename(m.group(1)), int(m.group(2)))
         continue
     if re.match(r'\s*/\*[0-9a-f]{4,}\*/', ln):
         lines.append(line)

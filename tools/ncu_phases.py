@@ -9,8 +9,13 @@ src = list(csv.reader(io.StringIO(subprocess.run(['ncu', '-i', rep, '--page', 's
 hdr = src[1]; rows = [dict(zip(hdr, x)) for x in src[2:]]
 with tempfile.TemporaryDirectory() as d:
     subprocess.run(['cuobjdump', '-xelf', 'all', obj], cwd=d, capture_output=True)
-    cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith('.cubin')][0]
-    dis = subprocess.run(['nvdisasm', '-g', '-c', cub], capture_output=True, text=True).stdout
+    dis = ''
+    for f in sorted(os.listdir(d)):  # the cubin that holds the kernel
+        if f.endswith('.cubin'):
+            t = subprocess.run(['nvdisasm', '-g', '-c', os.path.join(d, f)], capture_output=True, text=True).stdout
+            if ks in t:
+                dis = t
+                break
 funcs = re.split(r'\n\s*\.text\.(\S+):', dis)
 body = next(funcs[i + 1] for i in range(1, len(funcs), 2) if ks in funcs[i])
 line, lines = None, []
