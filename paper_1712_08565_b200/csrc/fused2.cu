@@ -161,6 +161,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
       "r"(parity));
 }
+__device__ __forceinline__ void bulk_load(double* dst, const double* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
@@ -170,9 +176,17 @@ __device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map,
 }
 
 // ---- the kernel ----------------------------------------------------------------
+// CTAs per SM: 2 where the register state (ring 3(p+1) + accumulators NT(p+3) doubles) fits
+// 128 registers without spilling, else 1 with up to 255 registers
+__host__ __device__ constexpr int occ_for(int p, int nt) {
+#ifdef MFWQ_OCC6
+  if (nt == 3 && p == MFWQ_OCCP) return MFWQ_OCC6;
+#endif
+  return ((nt == 3 && p <= 6) || (nt == 5 && p <= 2)) ? 2 : 1;
+}
 template <int P, int NT>
-struct Occ {  // 2 CTAs/SM where the register budget allows it
-  static constexpr int MINB = ((NT == 3 && P <= 6) || (NT == 5 && P <= 2)) ? 2 : 1;
+struct Occ {
+  static constexpr int MINB = occ_for(P, NT);
 };
 template <int NT>
 __host__ __device__ constexpr int n_xtypes() {
@@ -216,14 +230,16 @@ struct Smem {
   static constexpr int G = n_grids<NT>(), NX = n_xtypes<NT>(), NY = n_ytypes<NT>();
   static constexpr int CST = ZS * 2 * G * 256;                      // one TMA stage
   static constexpr int TSZ = ZS * NT * TQ * PK;                     // sT (aliases the consumed C stage)
-  static constexpr int ASZ = ZS * 2 * TQ * PV, SSZ = ZS * NT * TQ * PV;
+  static constexpr int ASZ = ZS * 2 * TQ * PV, SSZ = ZS * NY * TQ * PV;
   static constexpr int AS = ASZ > SSZ ? ASZ : SSZ;                  // sA / sS union
   static_assert(TSZ <= CST, "sT must fit in a coefficient stage");
   static constexpr int oC = 0, oBy = 2 * CST, oWx = oBy + 2 * TQ * PKB, oWy = oWx + NX * TQ * PV,
                        oV = oWy + NY * PV * PK, oAS = oV + ZS * PV * PV, oBx = oAS + AS, oZ = oBx + 2 * TQ * NB;
+  static constexpr int DMAX = TQ / 2 + P + 1;                      // DoF window bound
+  static constexpr int FPT = (DMAX * DMAX + NTHR - 1) / NTHR;       // v-window cells per thread
   static size_t bytes(int qe, int max_chunk) {
-    return sizeof(double) * (size_t)(oZ + 2 * ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + sizeof(int) * (max_chunk + 2) +
-           sizeof(int) * ((PV * PV + NTHR - 1) / NTHR) * NTHR;
+    return sizeof(double) * (size_t)(oZ + 2 * ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + 32 + sizeof(int) * (max_chunk + 2) +
+           sizeof(int) * FPT * NTHR + sizeof(int) * (max_chunk / 2 + 2);
   }
 };
 
@@ -234,7 +250,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   constexpr int NB = L::NB, NW = L::NW, NBP = L::NBP, NWP = L::NWP, ZT = L::ZT, G = L::G;
   constexpr int R = NB;                          // ring slots (B side): pushed right before use
   constexpr int A = NW + ZS - 1;                 // accumulator slots (W side)
-  constexpr int DMAX = TQ / 2 + P + 1;           // DoF window bound (8 elements + p + 1)
+  constexpr int DMAX = L::DMAX;                  // DoF window bound (8 elements + p + 1)
   constexpr int NTD = (DMAX + 7) / 8;            // 8-wide tiles over a window dimension
   constexpr int KB = ((DMAX + 3) / 4);           // k-steps over window rows (By)
   static_assert(DMAX <= PV, "window exceeds tile pitch");
@@ -248,13 +264,17 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   double* sWy = sm + L::oWy;     // [NY][PV][PK]              dense Wy(r, q2), used y-types
   double* sV = sm + L::oV;       // [ZS][PV][PV]              v plane windows
   double* sA = sm + L::oAS;      // [ZS][2][16][PV]           B-side y result   (union with sS)
-  double* sS = sm + L::oAS;      // [ZS][NT][16][PV]          W x results
+  double* sS = sm + L::oAS;      // [ZS][NY][16][PV]          W x results per y-factor group
   double* sBx = sm + L::oBx;     // [2][16][NB]
   double* sZ = sm + L::oZ;       // [2][ZS*QE][ZT]            z tables
   int* sEx = reinterpret_cast<int*>(sZ + 2 * ZS * QE * ZT);
   int* sEy = sEx + TQ;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sEy + TQ);
-  int* sQ0 = reinterpret_cast<int*>(mbar + 2);
+  // tile scalars live in shared memory (re-read after each barrier) instead of pinning
+  // registers across the whole z loop
+  struct TileInfo { int Dx, Dy, dax, day, nez, ea3, q0x, q0y; };
+  TileInfo* sInf = reinterpret_cast<TileInfo*>(mbar + 2);
+  int* sQ0 = reinterpret_cast<int*>(sInf + 1);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ql1 = tid & 15, ql2 = tid >> 4;
@@ -264,7 +284,6 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   const int Dx = tx.eb - tx.ea + P + 1, Dy = ty.eb - ty.ea + P + 1;
   const int dax = tx.ea - 2, day = ty.ea - 2;
   const int n1 = prm.n1, n2 = prm.n2;
-  const int m2 = prm.m[1];
   const int nez = tz.eb - tz.ea;
 
   // ---- one-time staging: bulk copies of the host-prepared operand blocks --------
@@ -288,6 +307,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     }
     for (int i = tid; i <= nez; i += NTHR) sQ0[i] = prm.q0z[tz.ea + i];
     if (tid == 0) {
+      *sInf = TileInfo{Dx, Dy, dax, day, nez, tz.ea, tx.q0, ty.q0};
       mbar_init(&mbar[0], 1);
       mbar_init(&mbar[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
@@ -314,39 +334,39 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 
   // v-plane window -> sV[z] (cp.async, zero fill outside the domain); caller commits.
   // Each thread owns fixed window cells: their in-plane offsets are computed once.
-  constexpr int FPT = (PV * PV + NTHR - 1) / NTHR;
-  int* sFP = sQ0 + (nez + 2);  // [FPT][NTHR] packed (global in-plane offset << 10 | window cell), -1 = zero
+  // Window cells outside the domain are never written (sV was zeroed once), so each thread
+  // keeps only its in-domain cells.
+  constexpr int FPT = L::FPT;
+  int* sFP = sQ0 + (nez + 2);  // [FPT][NTHR] packed (global in-plane offset << 10 | window cell), -1 = none
+  int* sStep = sFP + FPT * NTHR;  // per step of ZS elements: coefficient planes by TMA (1) or not (0)
   for (int k = 0; k < FPT; ++k) {
     const int e = tid + k * NTHR, r = e / Dx, c = e % Dx, g2 = day + r, g1 = dax + c;
-    const bool inwin = e < Dy * Dx, ok = inwin && g2 >= 0 && g2 < n2 && g1 >= 0 && g1 < n1;
-    sFP[k * NTHR + tid] = !inwin ? -2 : (ok ? ((g2 * n1 + g1) << 10) | (r * PV + c) : -1 - (((r * PV + c)) << 1));
+    const bool ok = e < Dy * Dx && g2 >= 0 && g2 < n2 && g1 >= 0 && g1 < n1;
+    sFP[k * NTHR + tid] = ok ? ((g2 * n1 + g1) << 10) | (r * PV + c) : -1;
   }
-  const size_t plane_sz = (size_t)n2 * n1;
   auto fetch_plane = [&](int i3, int z) {
     if (MFWQ_ABLATE == 5) return;
     const bool vp = i3 >= prm.v_lo && i3 < prm.v_hi;
     double* dst = sV + z * PV * PV;
-    const double* src = xv + (vp ? (size_t)(i3 - prm.v_lo) * plane_sz : 0);
+    const double* src = xv + (vp ? (size_t)(i3 - prm.v_lo) * prm.n2 * prm.n1 : 0);
 #pragma unroll
     for (int k = 0; k < FPT; ++k) {
       const int code = sFP[k * NTHR + tid];
-      if (code == -2) continue;
-      if (code >= 0) cp_async8(dst + (code & 1023), src + (code >> 10), vp);
-      else cp_async8(dst + ((-1 - code) >> 1), xv, false);  // outside the domain: zero
+      if (code >= 0) cp_async8(dst + (code & 1023), src + (code >> 10), vp);  // !vp: zero fill
     }
   };
-  // z tables of chunk elements [el, el+nz): one contiguous block of the flat [m3][ZT] table
-  auto fetch_ztab = [&](int el, int nz, int stage) {
-    if (MFWQ_ABLATE == 6) return;
-    double* dst = sZ + stage * ZS * QE * ZT;
-    const int qa = sQ0[el], n = (sQ0[el + nz] - qa) * ZT;
-    const double* src = prm.ztab + (size_t)qa * ZT;
-    for (int i = 2 * tid; i < n; i += 2 * NTHR) cp_async16(dst + i, src + i);
-  };
-  // coefficient planes of chunk elements [el, el+ZS) (2 planes each) -> sC[stage] by TMA
-  auto issue_coeff = [&](int el, int stage) {
+  // one stage transaction (thread 0): the z tables of chunk elements [el, el+nz) as one bulk
+  // copy of the flat [m3][ZT] table, plus (TMA steps) their coefficient planes -> sC[stage]
+  auto issue_stage = [&](int el, int nz, int stage) {
     if (tid == 0) {
-      mbar_expect_tx(&mbar[stage], ZS * G * 2 * TQ * TQ * 8);
+      // order earlier generic-proxy accesses of these buffers (sT, z rows) before the async writes
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      const bool tma = nz == ZS && sStep[el / ZS];
+      const int qa = sQ0[el];
+      const unsigned zbytes = (unsigned)((sQ0[el + nz] - qa) * ZT * 8);
+      mbar_expect_tx(&mbar[stage], zbytes + (tma ? ZS * G * 2 * TQ * TQ * 8 : 0));
+      bulk_load(sZ + stage * ZS * QE * ZT, prm.ztab + (size_t)qa * ZT, zbytes, &mbar[stage]);
+      if (!tma) return;
 #pragma unroll
       for (int ez = 0; ez < ZS; ++ez) {
         const int qa = sQ0[el + ez];
@@ -356,18 +376,18 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
           const int sl = grid_slot<NT>(g);
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl)
-            tma_load_3d(sC + stage * L::CST + ((ez * 2 + pl) * G + sl) * 256, &maps.m[g], tx.q0, ty.q0,
+            tma_load_3d(sC + stage * L::CST + ((ez * 2 + pl) * G + sl) * 256, &maps.m[g], sInf->q0x, sInf->q0y,
                         qa + pl - prm.qzb, &mbar[stage]);
         }
       }
     }
   };
-  auto all_two = [&](int el) {  // every element of the step has exactly 2 quadrature planes
-    bool ok = true;
-#pragma unroll
-    for (int ez = 0; ez < ZS; ++ez) ok = ok && (el + ez < nez) && (sQ0[el + ez + 1] - sQ0[el + ez] == 2);
-    return ok;
-  };
+  // a step takes its coefficients by TMA when it has ZS elements of exactly 2 planes each
+  for (int i = tid; i * ZS < nez; i += NTHR) {
+    bool ok = i * ZS + ZS <= nez;
+    for (int ez = 0; ez < ZS && ok; ++ez) ok = sQ0[i * ZS + ez + 1] - sQ0[i * ZS + ez] == 2;
+    sStep[i] = ok ? 1 : 0;
+  }
 
   // push one DoF plane (already contracted in y into sA[z]) through the x-contraction into the ring
   auto push_x = [&](int z) {
@@ -440,34 +460,26 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #if MFWQ_ABLATE == 1
     return;
 #endif
-    // x-contraction per (row, term): S(q2, c) = sum_ql T(q2, ql) Wx^T(ql, c)
+    // x-contraction per (row, y-factor group): S_g(q2, c) = sum_{t in g} sum_ql T_t(q2, ql) Wx_t^T(ql, c);
+    // the terms sharing a y-factor accumulate in one DMMA chain
     {
-      constexpr int NTASK = ne * NT * 2 * NTD, PER = (NTASK + NWARP - 1) / NWARP;
-      double d[PER][4];
+      constexpr int NY = L::NY, NTASK = ne * NY * 2 * NTD;
+      for (int task = warp; task < NTASK; task += NWARP) {
+        const int z = task / (NY * 2 * NTD), ys = (task / (2 * NTD)) % NY, mt = (task / NTD) % 2, nt = task % NTD;
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {  // independent tiles per warp, interleaved
-        const int task = warp + i * NWARP;
-        d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0;
-        if (NTASK % NWARP != 0 && task >= NTASK) continue;
-        const int z = task / (NT * 2 * NTD), t = (task / (2 * NTD)) % NT, mt = (task / NTD) % 2, nt = task % NTD;
-        int xs = 0;
-#pragma unroll
-        for (int u = 0; u < NT; ++u)
-          if (u == t) xs = xslot<NT>(wtype(T::a(u), T::b(u), 0));
-        const double* ap = sT + ((z * NT + t) * TQ + mt * 8 + (lane >> 2)) * PK + (lane & 3);
-        const double* bp = sWxT + (xs * TQ + (lane & 3)) * PV + nt * 8 + (lane >> 2);
-        dmma(d[i][0], d[i][1], ap[0], bp[0]);
-        dmma(d[i][2], d[i][3], ap[4], bp[4 * PV]);
-        dmma(d[i][0], d[i][1], ap[8], bp[8 * PV]);
-        dmma(d[i][2], d[i][3], ap[12], bp[12 * PV]);
-      }
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int task = warp + i * NWARP;
-        if (NTASK % NWARP != 0 && task >= NTASK) continue;
-        const int z = task / (NT * 2 * NTD), t = (task / (2 * NTD)) % NT, mt = (task / NTD) % 2, nt = task % NTD;
-        double* o = sS + ((z * NT + t) * TQ + mt * 8 + (lane >> 2)) * PV + nt * 8 + 2 * (lane & 3);
-        *reinterpret_cast<double2*>(o) = make_double2(d[i][0] + d[i][2], d[i][1] + d[i][3]);
+        for (int t = 0; t < NT; ++t) {
+          if (yslot<NT>(wtype(T::a(t), T::b(t), 1)) != ys) continue;  // warp-uniform
+          const int xs = xslot<NT>(wtype(T::a(t), T::b(t), 0));
+          const double* ap = sT + ((z * NT + t) * TQ + mt * 8 + (lane >> 2)) * PK + (lane & 3);
+          const double* bp = sWxT + (xs * TQ + (lane & 3)) * PV + nt * 8 + (lane >> 2);
+          dmma(d0, d1, ap[0], bp[0]);
+          dmma(e0, e1, ap[4], bp[4 * PV]);
+          dmma(d0, d1, ap[8], bp[8 * PV]);
+          dmma(e0, e1, ap[12], bp[12 * PV]);
+        }
+        double* o = sS + ((z * NY + ys) * TQ + mt * 8 + (lane >> 2)) * PV + nt * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(o) = make_double2(d0 + e0, d1 + e1);
       }
     }
     __syncthreads();
@@ -486,10 +498,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         for (int ks = 0; ks < 4; ++ks) {
           const int kq = ks * 4 + (lane & 3);
           const double a = sWy[(yslot<NT>(w) * PV + mt * 8 + (lane >> 2)) * PK + kq];
-          double bb = 0.0;
-#pragma unroll
-          for (int t = 0; t < NT; ++t)
-            if (wtype(T::a(t), T::b(t), 1) == w) bb += sS[((z * NT + t) * TQ + kq) * PV + nt * 8 + (lane >> 2)];
+          const double bb = sS[((z * L::NY + yslot<NT>(w)) * TQ + kq) * PV + nt * 8 + (lane >> 2)];
           if (chain++ & 1) dmma(e0, e1, a, bb);
           else dmma(d0, d1, a, bb);
         }
@@ -497,7 +506,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       d0 += e0;
       d1 += e1;
       const int r = mt * 8 + (lane >> 2), c = nt * 8 + 2 * (lane & 3);
-      const int g2 = day + r, g1 = dax + c;
+      const int n1 = prm.n1, n2 = prm.n2, Dx = sInf->Dx, Dy = sInf->Dy;
+      const int g2 = sInf->day + r, g1 = sInf->dax + c;
       const size_t plane = (size_t)(i3 - prm.y_lo) * n2;
       if (r < Dy && g2 >= 0 && g2 < n2) {
 #if MFWQ_ABLATE == 4  // timing experiment only: plain stores instead of atomics
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     for (int g = 0; g < 6; ++g) {
       if (!grid_used<NT>(g)) { cg[g] = 0.0; continue; }
       if constexpr (kTMA) cg[g] = active ? cst[grid_slot<NT>(g) * 256] : 0.0;
-      else cg[g] = active ? __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * m2 + ty.q0 + ql2) * prm.m1p + tx.q0 + ql1) : 0.0;
+      else cg[g] = active ? __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * prm.m[1] + sInf->q0y + ql2) * prm.m1p + sInf->q0x + ql1) : 0.0;
     }
     double tv[NT];
 #pragma unroll
@@ -580,29 +590,26 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     __syncthreads();
     push_x(0);
   }
-  // per-step TMA eligibility (every element of the step has exactly 2 planes)
-  auto step_tma = [&](int el) { return el + ZS <= nez && all_two(el); };
+  // first step: its DoF planes and its stage (z rows, coefficient planes)
   {
     const int nz0 = nez >= ZS ? ZS : 1;
     for (int z = 0; z < nz0; ++z) fetch_plane(tz.ea + P - 1 + z, z);
-    fetch_ztab(0, nez >= ZS ? ZS : 1, 0);
     cp_commit();
-    if (step_tma(0)) issue_coeff(0, 0);
+    issue_stage(0, nez >= ZS ? ZS : 1, 0);
   }
   unsigned parity = 0u;  // bit s: phase of mbar[s] (a register, not a local array)
 
   // one step over NZ (compile-time) z-elements starting at chunk element el, stage s
   auto do_step = [&](auto NZc, int el, int s) {
     constexpr int nz = decltype(NZc)::value;
-    const int e3 = tz.ea + el;
+    const int e3 = sInf->ea3 + el, nez = sInf->nez;
     cp_wait_all();
-    __syncthreads();  // sV, sZ[s] landed; step-1 finished with sC[s^1], sZ[s^1], sT/sS
+    __syncthreads();  // sV landed; step-1 finished with sC[s^1], sZ[s^1], sT/sS
     PROF(0)
     const int eln = el + nz;
     const int nzn = (nez - eln) >= ZS ? ZS : 1;
     if (eln < nez) {
-      fetch_ztab(eln, nzn, s ^ 1);
-      if (step_tma(eln)) issue_coeff(eln, s ^ 1);
+      issue_stage(eln, nzn, s ^ 1);
     }
     PROF(1)
     bside_y(nz);
@@ -612,10 +619,10 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       for (int z = 0; z < nzn; ++z) fetch_plane(e3 + nz + P - 1 + z, z);  // next step's planes
     cp_commit();
     const double* zt = sZ + s * ZS * QE * ZT;
-    if (nz == ZS && step_tma(el)) {
-      mbar_wait(&mbar[s], (parity >> s) & 1u);
-      parity ^= 1u << s;
-      PROF(4)
+    mbar_wait(&mbar[s], (parity >> s) & 1u);  // z rows (and TMA coefficient planes) landed
+    parity ^= 1u << s;
+    PROF(4)
+    if (nz == ZS && sStep[el / ZS]) {
       const double* cst = sC + s * L::CST + cthr;
 #pragma unroll
       for (int ez = 0; ez < nz; ++ez) {
@@ -639,12 +646,12 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   };
 
   int el = 0, step = 0;
-  for (; el + ZS <= nez; el += ZS, ++step) do_step(std::integral_constant<int, ZS>{}, el, step & 1);
-  if (el < nez) do_step(std::integral_constant<int, 1>{}, el, step & 1);  // odd tail
+  for (; el + ZS <= sInf->nez; el += ZS, ++step) do_step(std::integral_constant<int, ZS>{}, el, step & 1);
+  if (el < sInf->nez) do_step(std::integral_constant<int, 1>{}, el, step & 1);  // odd tail
   // flush the open planes (partial; neighbours add theirs): slot k holds interior row eb-2+k
   for (int k = 0; k < NW - 1; ++k) {
     __syncthreads();
-    emit_rows(std::integral_constant<int, 1>{}, sC, tz.eb - 2 + k);
+    emit_rows(std::integral_constant<int, 1>{}, sC, sInf->ea3 + sInf->nez - 2 + k);
   }
   PROF_DUMP
 }
@@ -719,7 +726,7 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
       const long long inplane = (long long)F->ntile[0] * F->ntile[1];
       const int mask = S.term_mask();
       const int nt = (mask & ~0x111) == 0 ? 3 : ((mask & ~0x11B) == 0 ? 5 : 9);
-      const int occ = (nt == 3 && p <= 6) || (nt == 5 && p <= 2) ? 2 : 1;
+      const int occ = f2::occ_for(p, nt);
       int dev = 0, nsm = 148;
       if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const long long slots = (long long)occ * nsm;
