@@ -228,17 +228,18 @@ struct Smem {
   static constexpr int NBP = (NB + 1) & ~1, NWP = (NW + 1) & ~1;  // 16-byte aligned sub-tables
   static constexpr int ZT = 2 * NBP + 4 * NWP;                     // z-table doubles per plane
   static constexpr int G = n_grids<NT>(), NX = n_xtypes<NT>(), NY = n_ytypes<NT>();
-  static constexpr int CST = ZS * 2 * G * 256;                      // one TMA stage
-  static constexpr int TSZ = ZS * NT * TQ * PK;                     // sT (aliases the consumed C stage)
-  static constexpr int ASZ = ZS * 2 * TQ * PV, SSZ = ZS * NY * TQ * PV;
-  static constexpr int AS = ASZ > SSZ ? ASZ : SSZ;                  // sA / sS union
-  static_assert(TSZ <= CST, "sT must fit in a coefficient stage");
-  static constexpr int oC = 0, oBy = 2 * CST, oWx = oBy + 2 * TQ * PKB, oWy = oWx + NX * TQ * PV,
-                       oV = oWy + NY * PV * PK, oAS = oV + ZS * PV * PV, oBx = oAS + AS, oZ = oBx + 2 * TQ * NB;
+  static constexpr int CST = ZS * 2 * G * 256;                      // the TMA coefficient stage
   static constexpr int DMAX = TQ / 2 + P + 1;                      // DoF window bound
+  static constexpr int KB = (DMAX + 3) / 4, VR = 4 * KB;           // By k-steps, v-window rows read
+  static constexpr int TSZ = ZS * NT * TQ * PK;                     // sT: emitted rows per term
+  static constexpr int ASZ = ZS * 2 * TQ * PV, SSZ = ZS * NY * TQ * PV;
+  // every buffer has its own space (no aliasing), so a step needs three CTA barriers
+  static constexpr int oC = 0, oT = CST, oBy = oT + TSZ, oWx = oBy + 2 * TQ * PKB, oWy = oWx + NX * TQ * PV,
+                       oV = oWy + NY * PV * PK, oA = oV + ZS * VR * PV, oS = oA + ASZ, oBx = oS + SSZ,
+                       oZ = oBx + 2 * TQ * NB;
   static constexpr int FPT = (DMAX * DMAX + NTHR - 1) / NTHR;       // v-window cells per thread
   static size_t bytes(int qe, int max_chunk) {
-    return sizeof(double) * (size_t)(oZ + 2 * ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + 32 + sizeof(int) * (max_chunk + 2) +
+    return sizeof(double) * (size_t)(oZ + ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + 32 + sizeof(int) * (max_chunk + 2) +
            sizeof(int) * FPT * NTHR + sizeof(int) * (max_chunk / 2 + 2);
   }
 };
@@ -249,25 +250,26 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   using L = Smem<P, NT, ZS>;
   constexpr int NB = L::NB, NW = L::NW, NBP = L::NBP, NWP = L::NWP, ZT = L::ZT, G = L::G;
   constexpr int R = NB;                          // ring slots (B side): pushed right before use
-  constexpr int A = NW + ZS - 1;                 // accumulator slots (W side)
+  constexpr int A = NW;                          // accumulator slots (W side): retired per element
   constexpr int DMAX = L::DMAX;                  // DoF window bound (8 elements + p + 1)
   constexpr int NTD = (DMAX + 7) / 8;            // 8-wide tiles over a window dimension
-  constexpr int KB = ((DMAX + 3) / 4);           // k-steps over window rows (By)
+  constexpr int KB = L::KB, VR = L::VR;          // k-steps over window rows (By), rows of a v window
   static_assert(DMAX <= PV, "window exceeds tile pitch");
   using T = Terms<NT>;
 
   const int QE = prm.qe;  // max quadrature planes per z-element
   extern __shared__ __align__(128) double sm[];
-  double* sC = sm + L::oC;       // [2][ZS*2 planes][G][256]  TMA stages
+  double* sC = sm + L::oC;       // [ZS*2 planes][G][256]     TMA coefficient stage
+  double* sT = sm + L::oT;       // [ZS][NT][16][PK]          emitted W rows (A operand of W x)
   double* sBy = sm + L::oBy;     // [2][16][PKB]              dense By(q2, r)
   double* sWxT = sm + L::oWx;    // [NX][16][PV]              dense Wx^T(ql, c), used x-types
   double* sWy = sm + L::oWy;     // [NY][PV][PK]              dense Wy(r, q2), used y-types
-  double* sV = sm + L::oV;       // [ZS][PV][PV]              v plane windows
-  double* sA = sm + L::oAS;      // [ZS][2][16][PV]           B-side y result   (union with sS)
-  double* sS = sm + L::oAS;      // [ZS][NY][16][PV]          W x results per y-factor group
+  double* sV = sm + L::oV;       // [ZS][VR][PV]              v plane windows
+  double* sA = sm + L::oA;       // [ZS][2][16][PV]           B-side y result
+  double* sS = sm + L::oS;       // [ZS][NY][16][PV]          W x results per y-factor group
   double* sBx = sm + L::oBx;     // [2][16][NB]
-  double* sZ = sm + L::oZ;       // [2][ZS*QE][ZT]            z tables
-  int* sEx = reinterpret_cast<int*>(sZ + 2 * ZS * QE * ZT);
+  double* sZ = sm + L::oZ;       // [ZS*QE][ZT]               z tables
+  int* sEx = reinterpret_cast<int*>(sZ + ZS * QE * ZT);
   int* sEy = sEx + TQ;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sEy + TQ);
   // tile scalars live in shared memory (re-read after each barrier) instead of pinning
@@ -309,10 +311,9 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     if (tid == 0) {
       *sInf = TileInfo{Dx, Dy, dax, day, nez, tz.ea, tx.q0, ty.q0};
       mbar_init(&mbar[0], 1);
-      mbar_init(&mbar[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
-    for (int i = tid; i < ZS * PV * PV; i += NTHR) sV[i] = 0.0;
+    for (int i = tid; i < ZS * VR * PV; i += NTHR) sV[i] = 0.0;
     cp_wait_all();
   }
   __syncthreads();
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   auto fetch_plane = [&](int i3, int z) {
     if (MFWQ_ABLATE == 5) return;
     const bool vp = i3 >= prm.v_lo && i3 < prm.v_hi;
-    double* dst = sV + z * PV * PV;
+    double* dst = sV + z * VR * PV;
     const double* src = xv + (vp ? (size_t)(i3 - prm.v_lo) * prm.n2 * prm.n1 : 0);
 #pragma unroll
     for (int k = 0; k < FPT; ++k) {
@@ -356,16 +357,17 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     }
   };
   // one stage transaction (thread 0): the z tables of chunk elements [el, el+nz) as one bulk
-  // copy of the flat [m3][ZT] table, plus (TMA steps) their coefficient planes -> sC[stage]
-  auto issue_stage = [&](int el, int nz, int stage) {
+  // copy of the flat [m3][ZT] table, plus (TMA steps) their coefficient planes -> sC
+  auto issue_stage = [&](int el, int nz) {
+    constexpr int stage = 0;
     if (tid == 0) {
-      // order earlier generic-proxy accesses of these buffers (sT, z rows) before the async writes
+      // order the previous step's generic-proxy reads of sC / sZ before the async overwrite
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       const bool tma = nz == ZS && sStep[el / ZS];
       const int qa = sQ0[el];
       const unsigned zbytes = (unsigned)((sQ0[el + nz] - qa) * ZT * 8);
       mbar_expect_tx(&mbar[stage], zbytes + (tma ? ZS * G * 2 * TQ * TQ * 8 : 0));
-      bulk_load(sZ + stage * ZS * QE * ZT, prm.ztab + (size_t)qa * ZT, zbytes, &mbar[stage]);
+      bulk_load(sZ, prm.ztab + (size_t)qa * ZT, zbytes, &mbar[stage]);
       if (!tma) return;
 #pragma unroll
       for (int ez = 0; ez < ZS; ++ez) {
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
           const int sl = grid_slot<NT>(g);
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl)
-            tma_load_3d(sC + stage * L::CST + ((ez * 2 + pl) * G + sl) * 256, &maps.m[g], sInf->q0x, sInf->q0y,
+            tma_load_3d(sC + ((ez * 2 + pl) * G + sl) * 256, &maps.m[g], sInf->q0x, sInf->q0y,
                         qa + pl - prm.qzb, &mbar[stage]);
         }
       }
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #pragma unroll
       for (int z = 0; z < ZS; ++z) {
         if (z >= nz) break;
-        const double* bp = sV + z * PV * PV + (lane & 3) * PV + nt * 8 + (lane >> 2);
+        const double* bp = sV + z * VR * PV + (lane & 3) * PV + nt * 8 + (lane >> 2);
         double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KB; ks += 2) {
@@ -438,28 +440,23 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     }
   };
 
-  // W side: emit accumulator slots 0..ne-1 as interior DoF planes i3s, i3s+1, ...; shift by ne
-  auto emit_rows = [&](auto NEc, double* sT, int i3s) {
-    constexpr int ne = decltype(NEc)::value;  // rows emitted (ZS in the main loop, 1 in tail/flush)
-    // sT must not be in use by anyone (caller syncs)
+  // W side: retire accumulator slot 0 (complete interior DoF plane) into sT row z and shift the
+  // accumulators by one; sT is free during the z-part (its reader, W x, ended before a barrier)
+  auto store_row = [&](int z) {
     double* st = sT + ql2 * PK + ql1;
 #pragma unroll
-    for (int z = 0; z < ne; ++z)
-#pragma unroll
-      for (int t = 0; t < NT; ++t) st[(z * NT + t) * TQ * PK] = active ? acc[t][z] : 0.0;
+    for (int t = 0; t < NT; ++t) st[(z * NT + t) * TQ * PK] = active ? acc[t][0] : 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
 #pragma unroll
-      for (int k = 0; k < A - ne; ++k) acc[t][k] = acc[t][k + ne];
-#pragma unroll
-      for (int k = A - ne; k < A; ++k) acc[t][k] = 0.0;
+      for (int k = 0; k < A - 1; ++k) acc[t][k] = acc[t][k + 1];
+      acc[t][A - 1] = 0.0;
     }
-    if (i3s + ne - 1 < prm.y_lo || i3s >= prm.y_hi) return;  // no valid row (CTA-uniform)
-    __syncthreads();
-    PROF(6)
-#if MFWQ_ABLATE == 1
-    return;
-#endif
+  };
+  auto rows_valid = [&](int ne, int i3s) { return !(i3s + ne - 1 < prm.y_lo || i3s >= prm.y_hi); };  // CTA-uniform
+  // W x (after the barrier that completes sT): sT -> sS
+  auto w_x = [&](auto NEc) {
+    constexpr int ne = decltype(NEc)::value;
     // x-contraction per (row, y-factor group): S_g(q2, c) = sum_{t in g} sum_ql T_t(q2, ql) Wx_t^T(ql, c);
     // the terms sharing a y-factor accumulate in one DMMA chain
     {
@@ -482,9 +479,10 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         *reinterpret_cast<double2*>(o) = make_double2(d0 + e0, d1 + e1);
       }
     }
-    __syncthreads();
-    PROF(7)
-    // y-contraction, summed over y-factor groups inside the K loop, then atomics
+  };
+  // W y (after the barrier that completes sS): sS -> w with fp64 atomics
+  auto w_y = [&](auto NEc, int i3s) {
+    constexpr int ne = decltype(NEc)::value;
     for (int task = warp; task < ne * NTD * NTD; task += NWARP) {
       const int z = task / (NTD * NTD), mt = (task / NTD) % NTD, nt = task % NTD;
       const int i3 = i3s + z;
@@ -590,46 +588,42 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     __syncthreads();
     push_x(0);
   }
-  // first step: its DoF planes and its stage (z rows, coefficient planes)
+  // first step: its DoF planes (y-contracted here) and its stage (z rows, coefficient planes)
   {
     const int nz0 = nez >= ZS ? ZS : 1;
     for (int z = 0; z < nz0; ++z) fetch_plane(tz.ea + P - 1 + z, z);
     cp_commit();
-    issue_stage(0, nez >= ZS ? ZS : 1, 0);
+    issue_stage(0, nz0);
+    cp_wait_all();
+    __syncthreads();
+    bside_y(nz0);
   }
-  unsigned parity = 0u;  // bit s: phase of mbar[s] (a register, not a local array)
+  unsigned parity = 0u;  // phase of the stage mbarrier
 
-  // one step over NZ (compile-time) z-elements starting at chunk element el, stage s
-  auto do_step = [&](auto NZc, int el, int s) {
+  // One step over NZ (compile-time) z-elements starting at chunk element el. Phases between the
+  // three barriers:  [B2] next v planes, z-part  [B3] next stage, W x  [B4] W y || next B-side y
+  auto do_step = [&](auto NZc, int el) {
     constexpr int nz = decltype(NZc)::value;
     const int e3 = sInf->ea3 + el, nez = sInf->nez;
-    cp_wait_all();
-    __syncthreads();  // sV landed; step-1 finished with sC[s^1], sZ[s^1], sT/sS
-    PROF(0)
     const int eln = el + nz;
     const int nzn = (nez - eln) >= ZS ? ZS : 1;
-    if (eln < nez) {
-      issue_stage(eln, nzn, s ^ 1);
-    }
-    PROF(1)
-    bside_y(nz);
-    __syncthreads();  // sA ready; sV free
-    PROF(2)
+    __syncthreads();  // B2: sA of this step complete, sV free
+    PROF(0)
     if (eln < nez)
       for (int z = 0; z < nzn; ++z) fetch_plane(e3 + nz + P - 1 + z, z);  // next step's planes
     cp_commit();
-    const double* zt = sZ + s * ZS * QE * ZT;
-    mbar_wait(&mbar[s], (parity >> s) & 1u);  // z rows (and TMA coefficient planes) landed
-    parity ^= 1u << s;
+    mbar_wait(&mbar[0], parity);  // z rows (and TMA coefficient planes) landed
+    parity ^= 1u;
     PROF(4)
     if (nz == ZS && sStep[el / ZS]) {
-      const double* cst = sC + s * L::CST + cthr;
+      const double* cst = sC + cthr;
 #pragma unroll
       for (int ez = 0; ez < nz; ++ez) {
         push_x(ez);  // ring: planes e3+ez-1 .. e3+ez+p-1, exactly the support of element e3+ez
 #pragma unroll
         for (int pl = 0; pl < 2; ++pl)
-          zpoint(std::true_type{}, 0, 0, ez, zt + (sQ0[el + ez] - sQ0[el] + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
+          zpoint(std::true_type{}, 0, 0, 0, sZ + (sQ0[el + ez] - sQ0[el] + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
+        store_row(ez);  // row e3+ez-2 complete
       }
     } else {  // boundary z-elements (extra planes) or the odd tail: C straight from global
 #pragma unroll
@@ -637,21 +631,38 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         push_x(ez);
         const int qa = sQ0[el + ez], nq = sQ0[el + ez + 1] - qa;
         for (int zl = 0; zl < nq; ++zl)
-          zpoint(std::false_type{}, qa + zl, 0, ez, zt + (qa - sQ0[el] + zl) * ZT, nullptr);
+          zpoint(std::false_type{}, qa + zl, 0, 0, sZ + (qa - sQ0[el] + zl) * ZT, nullptr);
+        store_row(ez);
       }
     }
     PROF(5)
-    __syncthreads();  // all reads of sC[s] done -> it becomes sT
-    emit_rows(std::integral_constant<int, nz>{}, sC + s * L::CST, e3 - 2);  // full rows e3-1.. complete
+    cp_wait_all();
+    __syncthreads();  // B3: sT complete, all reads of sC / sZ done, next v planes landed
+    PROF(6)
+    if (eln < nez) issue_stage(eln, nzn);
+    const bool rv = rows_valid(nz, e3 - 2);
+    if (rv) w_x(std::integral_constant<int, nz>{});
+    __syncthreads();  // B4: sS complete
+    PROF(7)
+    if (rv) w_y(std::integral_constant<int, nz>{}, e3 - 2);
+    if (eln < nez) {
+      if (nzn == ZS) bside_y(ZS);
+      else bside_y(1);
+    }
   };
 
-  int el = 0, step = 0;
-  for (; el + ZS <= sInf->nez; el += ZS, ++step) do_step(std::integral_constant<int, ZS>{}, el, step & 1);
-  if (el < sInf->nez) do_step(std::integral_constant<int, 1>{}, el, step & 1);  // odd tail
+  int el = 0;
+  for (; el + ZS <= sInf->nez; el += ZS) do_step(std::integral_constant<int, ZS>{}, el);
+  if (el < sInf->nez) do_step(std::integral_constant<int, 1>{}, el);  // odd tail
   // flush the open planes (partial; neighbours add theirs): slot k holds interior row eb-2+k
   for (int k = 0; k < NW - 1; ++k) {
+    const int i3 = sInf->ea3 + sInf->nez - 2 + k;
+    store_row(0);
     __syncthreads();
-    emit_rows(std::integral_constant<int, 1>{}, sC, sInf->ea3 + sInf->nez - 2 + k);
+    const bool rv = rows_valid(1, i3);
+    if (rv) w_x(std::integral_constant<int, 1>{});
+    __syncthreads();
+    if (rv) w_y(std::integral_constant<int, 1>{}, i3);
   }
   PROF_DUMP
 }
