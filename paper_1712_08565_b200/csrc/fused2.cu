@@ -461,7 +461,11 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     // the terms sharing a y-factor accumulate in one DMMA chain
     {
       constexpr int NY = L::NY, NTASK = ne * NY * 2 * NTD;
-      for (int task = warp; task < NTASK; task += NWARP) {
+      // round r hands warp w task r*8 + ((w + 4r) & 7): groups differ in chain length (a y-group
+      // holds 1..3 terms), and the rotation pairs long and short chains per warp
+      for (int r = 0; r * NWARP < NTASK; ++r) {
+        const int task = r * NWARP + ((warp + 4 * r) & (NWARP - 1));
+        if (task >= NTASK) continue;
         const int z = task / (NY * 2 * NTD), ys = (task / (2 * NTD)) % NY, mt = (task / NTD) % 2, nt = task % NTD;
         double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
