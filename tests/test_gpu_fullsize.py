@@ -28,3 +28,22 @@ def test_cfg2_matvec_anchor(p):
     scale = np.abs(y).max()
     assert np.abs(y[:8] - head).max() <= TOL[p] * 1e2 * scale
     assert np.abs(y[-8:] - tail).max() <= TOL[p] * 1e2 * scale
+
+
+# cfg 4 (k-method sweep, quarter ring, N = 128^3): ||u||_2 and iterations of the reference's own
+# FD-PCG run on b = default_rng(1) (SURVEY §8(c) anchors, 11 significant digits)
+CFG4 = {2: (128, 3.0208112873e+05, 27), 4: (126, 1.8017689318e+07, 27), 6: (124, 2.4482677025e+09, 28),
+        8: (122, 4.5817363209e+11, 31), 10: (120, 1.0585471769e+14, 33)}
+
+
+@pytest.mark.parametrize("p", [2, 4, 6, 8, 10])
+def test_cfg4_pcg_anchor(p):
+    n_el, unorm, iters = CFG4[p]
+    space = M.tensor_space(p, n_el)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map())
+    P = M.FDPreconditioner(space)
+    b = torch.from_numpy(np.random.default_rng(1).standard_normal(space.n_dofs)).cuda()
+    u, rep = M.cg(A.apply, b, P.apply, tol=1e-8)
+    assert rep.converged and abs(rep.iterations - iters) <= 1
+    # anchors carry 11 digits; the solution itself is reproduced to the PCG tolerance
+    assert abs(float(torch.linalg.vector_norm(u)) - unorm) <= 1e-9 * unorm
