@@ -137,8 +137,25 @@ int mfwq_pcg_solve(mfwq_stiffness_t A, mfwq_fd_t P, const double* b_dev, double*
 int mfwq_kron_apply(int d, const int* rows, const int* cols, const double* const* A_host, const double* x_dev,
                     double* y_dev, int accumulate, void* stream);
 
-/* device dot product (test helper) */
+/* device dot product a.b (deterministic two-level reduction), result on the host */
 int mfwq_dot(const double* a_dev, const double* b_dev, long long n, double* out, void* stream);
+
+/* ---- BiCGStab vector updates (solvers.py:176-249: bicgstab) ----------------------------------
+   The reference's iteration is host logic over numpy vector ops (solvers.py:198-248); these are the
+   fused device passes a binding calls in their place.  Reductions are returned to the host.      */
+/* aa_ab[0] = a.a, aa_ab[1] = a.b   (solvers.py:239-240: tt = t@t, t@s) */
+int mfwq_dot2(const double* a_dev, const double* b_dev, long long n, double* aa_ab, void* stream);
+/* y += a x   (solvers.py:233: x += alpha*phat at the early exit) */
+int mfwq_axpy(double* y_dev, const double* x_dev, long long n, double a, void* stream);
+/* p = r + beta (p - omega v)   (solvers.py:212) */
+int mfwq_bicg_p(double* p_dev, const double* r_dev, const double* v_dev, long long n, double beta, double omega,
+                void* stream);
+/* s = r - alpha v, *ss = ||s||^2   (solvers.py:230-231) */
+int mfwq_bicg_s(double* s_dev, const double* r_dev, const double* v_dev, long long n, double alpha, double* ss,
+                void* stream);
+/* x += alpha phat + omega shat ; r = s - omega t ; *rr = ||r||^2   (solvers.py:242-244) */
+int mfwq_bicg_xr(double* x_dev, double* r_dev, const double* phat_dev, const double* shat_dev, const double* s_dev,
+                 const double* t_dev, long long n, double alpha, double omega, double* rr, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ from .errors import (DegenerateGeometryError, EigenSolveError,
 from .geometry import GeometryMap, affine_map, identity_map, quarter_ring_map
 from .kron import CostMeter, kron_apply, tensor_grid
 from .operators import COEFF_EVAL_FLOPS, StiffnessOperator, setup_stiffness
-from .solvers import (FDPreconditioner, KrylovReport, cg, stopping_tolerance,
+from .solvers import (FDPreconditioner, KrylovReport, bicgstab, cg, stopping_tolerance,
                       univariate_parametric_matrices)
 from .splines import (KnotVector, TensorSpace, make_uniform_knots,
                       multi_to_scalar, scalar_to_multi, tensor_space)

@@ -64,6 +64,12 @@ _SIGS = {
     "mfwq_pcg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
                                  dp, C.POINTER(KrylovReportC), C.c_void_p]),
     "mfwq_dot": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, dp, C.c_void_p]),
+    "mfwq_dot2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, dp, C.c_void_p]),
+    "mfwq_axpy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, C.c_double, C.c_void_p]),
+    "mfwq_bicg_p": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_double, C.c_double, C.c_void_p]),
+    "mfwq_bicg_s": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_double, dp, C.c_void_p]),
+    "mfwq_bicg_xr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong,
+                               C.c_double, C.c_double, dp, C.c_void_p]),
     "mfwq_kron_apply": (C.c_int, [C.c_int, ip, ip, C.POINTER(dp), C.c_void_p, C.c_void_p, C.c_int,
                                   C.c_void_p]),
 }

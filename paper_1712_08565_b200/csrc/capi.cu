@@ -234,7 +234,28 @@ int mfwq_kron_apply(int d, const int* rows, const int* cols, const double* const
 }
 
 int mfwq_dot(const double* a, const double* b, long long n, double* out, void* stream) {
-  return guard([&] { *out = dev_dot(a, b, n, (cudaStream_t)stream); });
+  return guard([&] { *out = dot_fast(a, b, n, (cudaStream_t)stream); });
+}
+
+int mfwq_dot2(const double* a, const double* b, long long n, double* aa_ab, void* stream) {
+  return guard([&] { dot2(a, b, n, aa_ab, (cudaStream_t)stream); });
+}
+
+int mfwq_axpy(double* y, const double* x, long long n, double a, void* stream) {
+  return guard([&] { axpy(y, x, n, a, (cudaStream_t)stream); });
+}
+
+int mfwq_bicg_p(double* p, const double* r, const double* v, long long n, double beta, double omega, void* stream) {
+  return guard([&] { bicg_p(p, r, v, n, beta, omega, (cudaStream_t)stream); });
+}
+
+int mfwq_bicg_s(double* s, const double* r, const double* v, long long n, double alpha, double* ss, void* stream) {
+  return guard([&] { *ss = bicg_s(s, r, v, n, alpha, (cudaStream_t)stream); });
+}
+
+int mfwq_bicg_xr(double* x, double* r, const double* phat, const double* shat, const double* s, const double* t,
+                 long long n, double alpha, double omega, double* rr, void* stream) {
+  return guard([&] { *rr = bicg_xr(x, r, phat, shat, s, t, n, alpha, omega, (cudaStream_t)stream); });
 }
 
 }  // extern "C"

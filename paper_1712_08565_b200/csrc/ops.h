@@ -107,4 +107,13 @@ void kron_apply_dense(int d, const int* rows, const int* cols, const double* con
 // vector kernels
 double dev_dot(const double* a, const double* b, long long N, cudaStream_t s);
 
+// BiCGStab fused vector updates (bicgstab.cu; solvers.py:176-249); reductions return to the host
+void bicg_p(double* p, const double* r, const double* v, long long N, double beta, double omega, cudaStream_t s);
+double bicg_s(double* sv, const double* r, const double* v, long long N, double alpha, cudaStream_t s);
+void dot2(const double* a, const double* b, long long N, double* aa_ab, cudaStream_t s);
+double dot_fast(const double* a, const double* b, long long N, cudaStream_t s);
+double bicg_xr(double* x, double* r, const double* ph, const double* sh, const double* sv, const double* t, long long N,
+               double alpha, double omega, cudaStream_t s);
+void axpy(double* y, const double* x, long long N, double a, cudaStream_t s);
+
 }  // namespace mfwq

@@ -202,3 +202,130 @@ def _cg_callables(apply_A, b, apply_P, tol, maxit):
         p = z + (rz_new / rz) * p
         rz = rz_new
     return _dev.back(x, host), KrylovReport(maxit, hist, False, matvecs, precs)
+
+
+def bicgstab(apply_A, b, apply_P=None, tol=1e-8, maxit=1000, seed=0):
+    """Right-preconditioned BiCGStab, true-residual history (solvers.py:176-249).
+
+    The control flow (breakdown tests, the one seeded restart, stopping) is the
+    reference's, taken on host scalars; every vector update is a fused device pass
+    (``mfwq_bicg_*``, csrc/bicgstab.cu).  When ``apply_A`` / ``apply_P`` are this
+    package's operators they write into persistent device buffers; other callables
+    are called with device vectors (numpy callables with host copies), like ``cg``.
+    The restart shadow ``r + 1e-8 |b| N(0,1)`` is drawn from numpy's
+    ``default_rng(seed)`` (``seed + 1`` for the r~.v breakdown) as in the reference.
+    """
+    import torch
+
+    from .operators import StiffnessOperator
+
+    bt, host = _dev.to_device(b)
+    n = bt.numel()
+    L = _lib.lib()
+    st = C.c_void_p(_dev.stream_ptr())
+
+    def ptr(t):
+        return C.c_void_p(t.data_ptr())
+
+    def dot(a, c):
+        out = C.c_double()
+        _lib.check(L.mfwq_dot(ptr(a), ptr(c), n, C.byref(out), st))
+        return out.value
+
+    A_op = _bound_op(apply_A, StiffnessOperator)
+    P_op = _bound_op(apply_P, FDPreconditioner) if apply_P is not None else None
+    np_callables = host is True  # numpy in -> user callables expect numpy
+
+    def op(f, fop, v, out):
+        if fop is not None:
+            return fop.apply(v, out=out)
+        if np_callables:
+            return _dev.to_device(f(v.cpu().numpy()), n)[0]
+        return _dev.to_device(f(v), n)[0]
+
+    def A(v, out):
+        return op(apply_A, A_op, v, out)
+
+    def P(v, out):
+        if apply_P is None:
+            out.copy_(v)
+            return out
+        return op(apply_P, P_op, v, out)
+
+    x = torch.zeros_like(bt)
+    bnorm = float(np.sqrt(dot(bt, bt)))
+    if bnorm == 0.0:
+        return _dev.back(x, host), KrylovReport(0, [0.0], True, 0, 0)
+    eps = np.finfo(float).eps
+    work = torch.empty((7, n), dtype=torch.float64, device=bt.device)
+    v, p, ph, s, sh, t, tmp = work
+    r = bt - A(x, tmp)
+    matvecs, precs, restarted = 1, 0, False
+    residuals = [1.0]
+    r_shadow = r.clone()
+    rho = alpha = omega = 1.0
+    v.zero_()
+    p.zero_()
+
+    def restart(sd):
+        noise = np.random.default_rng(sd).standard_normal(n)
+        return r + (1e-8 * bnorm) * torch.from_numpy(noise).to(r.device)
+
+    def finish(k, ok):
+        return _dev.back(x, host), KrylovReport(k, residuals, ok, matvecs, precs)
+
+    k = 0
+    while k < maxit:
+        k += 1
+        rho_new = dot(r_shadow, r)
+        if abs(rho_new) < eps * bnorm ** 2 or abs(omega) < eps:
+            if restarted:
+                return finish(k, False)
+            restarted = True
+            r_shadow = restart(seed)
+            rho = alpha = omega = 1.0
+            v.zero_()
+            p.zero_()
+            continue
+        beta = (rho_new / rho) * (alpha / omega)
+        rho = rho_new
+        _lib.check(L.mfwq_bicg_p(ptr(p), ptr(r), ptr(v), n, beta, omega, st))
+        phv = P(p, ph)
+        precs += 1
+        vv = A(phv, v)
+        if vv.data_ptr() != v.data_ptr():
+            v.copy_(vv)
+        matvecs += 1
+        denom = dot(r_shadow, v)
+        if abs(denom) < eps * bnorm ** 2:
+            if restarted:
+                return finish(k, False)
+            restarted = True
+            r_shadow = restart(seed + 1)
+            rho = alpha = omega = 1.0
+            v.zero_()
+            p.zero_()
+            continue
+        alpha = rho / denom
+        ss = C.c_double()
+        _lib.check(L.mfwq_bicg_s(ptr(s), ptr(r), ptr(v), n, alpha, C.byref(ss), st))
+        if np.sqrt(ss.value) / bnorm <= tol:
+            _lib.check(L.mfwq_axpy(ptr(x), ptr(phv), n, alpha, st))
+            residuals.append(float(np.sqrt(ss.value) / bnorm))
+            return finish(k, True)
+        shv = P(s, sh)
+        precs += 1
+        tv = A(shv, t)
+        matvecs += 1
+        tt_ts = (C.c_double * 2)()
+        _lib.check(L.mfwq_dot2(ptr(tv), ptr(s), n, tt_ts, st))
+        tt, ts = tt_ts[0], tt_ts[1]
+        omega = ts / tt if tt > 0 else 0.0
+        rr = C.c_double()
+        _lib.check(L.mfwq_bicg_xr(ptr(x), ptr(r), ptr(phv), ptr(shv), ptr(s), ptr(tv), n, alpha, omega,
+                                  C.byref(rr), st))
+        rel = float(np.sqrt(rr.value) / bnorm)
+        residuals.append(rel)
+        if rel <= tol:
+            return finish(k, True)
+    return finish(maxit, False)

@@ -58,3 +58,26 @@ def test_fd_and_pcg_match_reference(golden):
         assert abs(it - int(g["iters"])) <= 1
         assert np.linalg.norm(u - g["u"]) <= 1e-9 * np.linalg.norm(g["u"])
         assert (nmv, npc) == (int(g["matvecs"]), int(g["precs"])) or abs(it - int(g["iters"])) == 1
+
+
+def test_bicgstab_matches_reference():
+    """Oracle BiCGStab (restating solvers.py:176-249) vs the reference's own runs, including the
+    breakdown -> seeded restart -> failure path on a skew operator."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "solvers", "bicgstab_golden.npz"))
+    from conftest import load_golden
+    g = load_golden("ring_p3_n8")
+    kv, _, _, A = _oracle_problem(g)
+    P = O.FD([kv] * 3)
+    b = np.random.default_rng(1).standard_normal(A.N)
+    cases = {"ring_fd": (A.apply, b, P.apply, {}), "ring_nop_maxit5": (A.apply, b, None, {"maxit": 5}),
+             "skew": (O.skew_blocks(64), z["skew_b"], None, {})}
+    for tag, (op, rhs, pre, kw) in cases.items():
+        x, it, hist, conv, nmv, npc = O.bicgstab(op, rhs, pre, tol=1e-8, **kw)
+        meta = z[f"{tag}_meta"]
+        assert [it, int(conv), nmv, npc] == meta.tolist(), tag
+        ref_hist = z[f"{tag}_hist"]
+        assert len(hist) == len(ref_hist)
+        assert np.allclose(hist, ref_hist, rtol=1e-6, atol=1e-12), tag
+        xr = z[f"{tag}_x"]
+        assert np.linalg.norm(x - xr) <= 1e-9 * max(np.linalg.norm(xr), 1e-300), tag
