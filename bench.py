@@ -280,6 +280,26 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = dofs_step * e2e_steps * world / (float(e2e_t) * 1e-3)
 
+    # on-the-fly coefficients (reference on_the_fly=True, operators.py:171-183): same sweep with C
+    # evaluated in-kernel from C(xi1) instead of read from the N_q grids (secondary figure)
+    otf_us = {}
+    for p in SWEEP:
+        o = ops[p]
+        o["A"].set_on_the_fly(True)
+        for _ in range(2):
+            o["A"].apply(o["x"], out=o["y"])
+        ts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            e0.record(stream)
+            o["A"].apply(o["x"], out=o["y"])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        otf_us[p] = statistics.median(ts)
+        o["A"].set_on_the_fly(False)
+    otf = {"value": dofs_step / (sum(otf_us.values()) * 1e-6), "unit": UNIT, "per_degree_us": otf_us,
+           "note": "on_the_fly=True: C evaluated in-kernel from C(xi1), no N_q coefficient grids stored or read"}
+
     # roofline of the matvec kernel, aggregated over the sweep
     pk = peaks()
     med = {p: statistics.median(per_p[p]) for p in SWEEP}
@@ -300,6 +320,8 @@ def run_ours(args, rank, world, local):
     pcg = None
     if args.pcg and world == 1:
         pcg = run_pcg(M, torch, dev)
+        pcg["on_the_fly_variant"] = {k: v for k, v in run_pcg(M, torch, dev, otf=True).items()
+                                     if k in ("iterations", "converged", "solve_s", "u_norm", "device_memory_used_gb")}
     elif args.pcg:
         pcg = run_dist_pcg(M, torch, dev, rank, world)
 
@@ -327,6 +349,7 @@ def run_ours(args, rank, world, local):
                         "h2d_bytes_per_step": 8 * dofs_step, "d2h_bytes_per_step": 8 * dofs_step},
                 "gpu_launches": int(launches),
                 "clocks": clk.summary(),
+                "on_the_fly": otf,
                 "pcg": pcg}
         print(json.dumps(line), flush=True)
 
@@ -364,13 +387,14 @@ def run_dist_pcg(M, torch, dev, rank, world):
             "u_norm": float(nrm[0]) ** 0.5}
 
 
-def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1):
+def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1, otf=False):
     """Setup phases + FD-PCG to 1e-8 on b ~ N(0,1) seed 1, each phase timed (SURVEY §8(d) cfg 3-5)."""
     t0 = time.perf_counter()
     space = M.tensor_space(p, n_el)
     rule = M.build_tensor_rule(space)
     t1 = time.perf_counter()
-    A = M.setup_stiffness(space, rule, M.quarter_ring_map() if geom == "ring" else M.identity_map(3))
+    A = M.setup_stiffness(space, rule, M.quarter_ring_map() if geom == "ring" else M.identity_map(3),
+                          on_the_fly=otf)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     P = M.FDPreconditioner(space)
@@ -390,7 +414,7 @@ def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1):
         secs.append(e0.elapsed_time(e1) * 1e-3)
     sec = sorted(secs)[len(secs) // 2]
     free, total = torch.cuda.mem_get_info()
-    return {"device_memory_used_gb": (total - free) / 1e9, "config": f"quarter ring p={p} n_el={n_el}" if geom == "ring" else f"cube p={p} n_el={n_el}",
+    return {"device_memory_used_gb": (total - free) / 1e9, "on_the_fly": otf, "config": f"quarter ring p={p} n_el={n_el}" if geom == "ring" else f"cube p={p} n_el={n_el}",
             "N": space.n_dofs, "iterations": rep.iterations, "converged": rep.converged,
             "final_rel_residual": rep.residuals[-1], "solve_s": sec,
             "dof_iters_per_s": space.n_dofs * rep.iterations / sec,
@@ -398,9 +422,9 @@ def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1):
             "u_norm": float(torch.linalg.vector_norm(u))}
 
 
-def run_pcg(M, torch, dev):
+def run_pcg(M, torch, dev, otf=False):
     """cfg 3: quarter ring, p=4, n_el=256 (17.2 M DoFs), FD-PCG to 1e-8 on b ~ N(0,1) seed 1."""
-    r = solve_case(M, torch, dev, 4, 256)
+    r = solve_case(M, torch, dev, 4, 256, otf=otf)
     r["config"] = "cfg3 quarter ring p=4 n_el=256"
     return r
 

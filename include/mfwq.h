@@ -19,6 +19,8 @@
  *   mfwq_fd_create         FDPreconditioner.__init__                   solvers.py:72-101
  *   mfwq_fd_apply          FDPreconditioner.apply                      solvers.py:107-115
  *   mfwq_pcg_solve         cg (device-resident loop)                   solvers.py:137-173
+ *   mfwq_bicg_*, mfwq_dot2 bicgstab vector updates                     solvers.py:176-249
+ *   mfwq_stiffness_set_on_the_fly  on_the_fly=True coefficient mode    operators.py:171-183, 207-220
  */
 #ifndef MFWQ_H_
 #define MFWQ_H_
@@ -83,6 +85,12 @@ int mfwq_stiffness_create(const mfwq_stiffness_desc* d, mfwq_stiffness_t* out);
    (Nq,3,3) per-point diffusion or NULL.  Raises MFWQ_E_DEGENERATE if det J <= 0. */
 int mfwq_stiffness_set_geometry(mfwq_stiffness_t h, int kind, const double* affine9, const double* K9,
                                 const double* J_dev, const double* Kfield_dev, void* stream);
+/* on-the-fly coefficients (operators.py:138, 171-183, 207-220: on_the_fly=True): no N_q grids are
+   stored; the kernel evaluates C at the quadrature points from C(xi1), which is exact for the
+   analytic maps (identity / affine with constant K, quarter ring with K = I).  Other geometries
+   return MFWQ_E_NOTIMPL.  A later set_geometry / set_coeffs returns to stored grids. */
+int mfwq_stiffness_set_on_the_fly(mfwq_stiffness_t h, int kind, const double* affine9, const double* K9,
+                                  void* stream);
 /* six device grids (a<=b order 00,01,02,11,12,22), each (m3,m2,m1) contiguous */
 int mfwq_stiffness_set_coeffs(mfwq_stiffness_t h, const double* const* grids6_dev, void* stream);
 int mfwq_stiffness_get_coeff(mfwq_stiffness_t h, int key, double* out_dev, void* stream);

@@ -44,6 +44,7 @@ _SIGS = {
     "mfwq_univariate_km": (C.c_int, [C.c_int, C.c_int, dp, dp, dp]),
     "mfwq_stiffness_create": (C.c_int, [C.POINTER(StiffnessDesc), C.POINTER(C.c_void_p)]),
     "mfwq_stiffness_set_geometry": (C.c_int, [C.c_void_p, C.c_int, dp, dp, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mfwq_stiffness_set_on_the_fly": (C.c_int, [C.c_void_p, C.c_int, dp, dp, C.c_void_p]),
     "mfwq_stiffness_set_coeffs": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]),
     "mfwq_stiffness_get_coeff": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "mfwq_stiffness_sizes": (C.c_int, [C.c_void_p, ip, ip, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),

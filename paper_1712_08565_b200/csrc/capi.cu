@@ -117,6 +117,14 @@ int mfwq_stiffness_set_geometry(mfwq_stiffness_t h, int kind, const double* affi
   });
 }
 
+int mfwq_stiffness_set_on_the_fly(mfwq_stiffness_t h, int kind, const double* affine9, const double* K9,
+                                  void* stream) {
+  return guard([&] {
+    if (kind < 0 || kind > 3) throw ValueErr("unknown geometry kind");
+    h->op.set_on_the_fly(kind, affine9, K9, (cudaStream_t)stream);
+  });
+}
+
 int mfwq_stiffness_set_coeffs(mfwq_stiffness_t h, const double* const* grids, void* stream) {
   return guard([&] { h->op.set_coeffs(grids, (cudaStream_t)stream); });
 }

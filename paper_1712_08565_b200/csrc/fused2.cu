@@ -88,6 +88,7 @@ struct Params {
   const int* exy;   // [ntx][16] then [nty][16]
   const double* ztab;
   int xblk_sz, yblk_sz;
+  const double* cx;  // on-the-fly mode: C_g(xi1) table [6][m1]
 };
 
 struct Maps {
@@ -222,13 +223,13 @@ __host__ __device__ constexpr int yslot(int w) {
 }
 
 // shared-memory plan (doubles), shared by kernel and host launch code
-template <int P, int NT, int ZS>
+template <int P, int NT, int ZS, bool OTF>
 struct Smem {
   static constexpr int NB = P + 1, NW = P + 2;
   static constexpr int NBP = (NB + 1) & ~1, NWP = (NW + 1) & ~1;  // 16-byte aligned sub-tables
   static constexpr int ZT = 2 * NBP + 4 * NWP;                     // z-table doubles per plane
   static constexpr int G = n_grids<NT>(), NX = n_xtypes<NT>(), NY = n_ytypes<NT>();
-  static constexpr int CST = ZS * 2 * G * 256;                      // the TMA coefficient stage
+  static constexpr int CST = OTF ? 0 : ZS * 2 * G * 256;            // the TMA coefficient stage
   static constexpr int DMAX = TQ / 2 + P + 1;                      // DoF window bound
   static constexpr int KB = (DMAX + 3) / 4, VR = 4 * KB;           // By k-steps, v-window rows read
   static constexpr int TSZ = ZS * NT * TQ * PK;                     // sT: emitted rows per term
@@ -236,7 +237,7 @@ struct Smem {
   // every buffer has its own space (no aliasing), so a step needs three CTA barriers
   static constexpr int oC = 0, oT = CST, oBy = oT + TSZ, oWx = oBy + 2 * TQ * PKB, oWy = oWx + NX * TQ * PV,
                        oV = oWy + NY * PV * PK, oA = oV + ZS * VR * PV, oS = oA + ASZ, oBx = oS + SSZ,
-                       oZ = oBx + 2 * TQ * NB;
+                       oCx = oBx + 2 * TQ * NB, oZ = oCx + (OTF ? G * TQ : 0);
   static constexpr int FPT = (DMAX * DMAX + NTHR - 1) / NTHR;       // v-window cells per thread
   static size_t bytes(int qe, int max_chunk) {
     return sizeof(double) * (size_t)(oZ + ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + 32 + sizeof(int) * (max_chunk + 2) +
@@ -244,10 +245,10 @@ struct Smem {
   }
 };
 
-template <int P, int NT, int ZS>
+template <int P, int NT, int ZS, bool OTF>
 __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     k_fused(const __grid_constant__ Params prm, const __grid_constant__ Maps maps) {
-  using L = Smem<P, NT, ZS>;
+  using L = Smem<P, NT, ZS, OTF>;
   constexpr int NB = L::NB, NW = L::NW, NBP = L::NBP, NWP = L::NWP, ZT = L::ZT, G = L::G;
   constexpr int R = NB;                          // ring slots (B side): pushed right before use
   constexpr int A = NW;                          // accumulator slots (W side): retired per element
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   double* sA = sm + L::oA;       // [ZS][2][16][PV]           B-side y result
   double* sS = sm + L::oS;       // [ZS][NY][16][PV]          W x results per y-factor group
   double* sBx = sm + L::oBx;     // [2][16][NB]
+  double* sCx = sm + L::oCx;     // [G][16]                   on-the-fly C(xi1) of the tile's x-points
   double* sZ = sm + L::oZ;       // [ZS*QE][ZT]               z tables
   int* sEx = reinterpret_cast<int*>(sZ + ZS * QE * ZT);
   int* sEy = sEx + TQ;
@@ -314,6 +316,12 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
     for (int i = tid; i < ZS * VR * PV; i += NTHR) sV[i] = 0.0;
+    if constexpr (OTF) {
+#pragma unroll
+      for (int g = 0; g < 6; ++g)
+        if (grid_used<NT>(g) && tid < TQ)
+          sCx[grid_slot<NT>(g) * TQ + tid] = tid < tx.nq ? prm.cx[(size_t)g * prm.m[0] + tx.q0 + tid] : 0.0;
+    }
     cp_wait_all();
   }
   __syncthreads();
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     if (tid == 0) {
       // order the previous step's generic-proxy reads of sC / sZ before the async overwrite
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      const bool tma = nz == ZS && sStep[el / ZS];
+      const bool tma = !OTF && nz == ZS && sStep[el / ZS];
       const int qa = sQ0[el];
       const unsigned zbytes = (unsigned)((sQ0[el + nz] - qa) * ZT * 8);
       mbar_expect_tx(&mbar[stage], zbytes + (tma ? ZS * G * 2 * TQ * TQ * 8 : 0));
@@ -552,7 +560,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #pragma unroll
     for (int g = 0; g < 6; ++g) {
       if (!grid_used<NT>(g)) { cg[g] = 0.0; continue; }
-      if constexpr (kTMA) cg[g] = active ? cst[grid_slot<NT>(g) * 256] : 0.0;
+      if constexpr (OTF) cg[g] = active ? sCx[grid_slot<NT>(g) * TQ + ql1] : 0.0;
+      else if constexpr (kTMA) cg[g] = active ? cst[grid_slot<NT>(g) * 256] : 0.0;
       else cg[g] = active ? __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * prm.m[1] + sInf->q0y + ql2) * prm.m1p + sInf->q0x + ql1) : 0.0;
     }
     double tv[NT];
@@ -692,6 +701,7 @@ struct Fused2Plan {
 
 bool build_elem_tables(const Dir1D& d, std::vector<double>& B, std::vector<double>& W, std::vector<int>& eq);
 
+#ifndef MFWQ_F2_OTF_UNIT  // plan + tensor maps: defined once (fused2.cu), not in fused2_otf.cu
 static std::vector<f2::Tile> f2_tiles_inplane(const Dir1D& d) {
   // greedy element-aligned tiles of <= 16 quadrature points from element 0: with an even
   // number of boundary extras every tile but the last is exactly 16 points wide, so the
@@ -839,7 +849,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static void encode_maps(Stiffness& S, Fused2Plan& F) {
+void encode_maps(Stiffness& S, Fused2Plan& F) {
   if (F.maps_for == S.coeff.ptr) return;
   auto enc = get_encode();
   const size_t G = S.grid_elems();
@@ -856,11 +866,15 @@ static void encode_maps(Stiffness& S, Fused2Plan& F) {
   F.maps_for = S.coeff.ptr;
 }
 
-template <int P, int NT>
+#endif
+
+void encode_maps(Stiffness& S, Fused2Plan& F);
+
+template <int P, int NT, bool OTF>
 static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
   constexpr int ZS = 2;
   using namespace f2;
-  encode_maps(S, F);
+  if constexpr (!OTF) encode_maps(S, F);
   Params prm;
   for (int l = 0; l < 3; ++l) {
     prm.B[l] = F.B[l].ptr;
@@ -895,8 +909,9 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   prm.n2 = S.dir[1].n;
   prm.n3 = S.dir[2].n;
   prm.qe = F.qe;
-  const size_t smem = Smem<P, NT, ZS>::bytes(F.qe, F.max_chunk);
-  auto kern = k_fused<P, NT, ZS>;
+  prm.cx = S.cx.ptr;
+  const size_t smem = Smem<P, NT, ZS, OTF>::bytes(F.qe, F.max_chunk);
+  auto kern = k_fused<P, NT, ZS, OTF>;
   MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   MFWQ_CUDA(cudaMemsetAsync(y, 0, S.out_elems() * sizeof(double), s));
   dim3 grid(F.ntile[0] * F.ntile[1], F.ntile[2]);
@@ -904,36 +919,50 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   MFWQ_CUDA(cudaGetLastError());
 }
 
-template <int P>
+template <int P, bool OTF>
 static void dispatch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
   const int mask = S.term_mask();
-  if ((mask & ~0x111) == 0) launch2<P, 3>(S, F, x, y, s);
-  else if ((mask & ~0x11B) == 0) launch2<P, 5>(S, F, x, y, s);
-  else launch2<P, 9>(S, F, x, y, s);
+  if ((mask & ~0x111) == 0) launch2<P, 3, OTF>(S, F, x, y, s);
+  else if ((mask & ~0x11B) == 0) launch2<P, 5, OTF>(S, F, x, y, s);
+  else launch2<P, 9, OTF>(S, F, x, y, s);
 }
 
-bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s) {
-  Fused2Plan* F = fused2_plan(S);
-  if (!F->ok) return false;
+template <bool OTF>
+static bool dispatch_p(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
 #ifdef MFWQ_ONLY_P  // static-analysis builds of one degree (tools/sass_stats.sh); never in the product
-  if (F->p != MFWQ_ONLY_P) return false;
-  dispatch2<MFWQ_ONLY_P>(S, *F, x, y, s);
+  if (F.p != MFWQ_ONLY_P) return false;
+  dispatch2<MFWQ_ONLY_P, OTF>(S, F, x, y, s);
   return true;
 #endif
-  switch (F->p) {
-    case 1: dispatch2<1>(S, *F, x, y, s); break;
-    case 2: dispatch2<2>(S, *F, x, y, s); break;
-    case 3: dispatch2<3>(S, *F, x, y, s); break;
-    case 4: dispatch2<4>(S, *F, x, y, s); break;
-    case 5: dispatch2<5>(S, *F, x, y, s); break;
-    case 6: dispatch2<6>(S, *F, x, y, s); break;
-    case 7: dispatch2<7>(S, *F, x, y, s); break;
-    case 8: dispatch2<8>(S, *F, x, y, s); break;
-    case 9: dispatch2<9>(S, *F, x, y, s); break;
-    case 10: dispatch2<10>(S, *F, x, y, s); break;
+  switch (F.p) {
+    case 1: dispatch2<1, OTF>(S, F, x, y, s); break;
+    case 2: dispatch2<2, OTF>(S, F, x, y, s); break;
+    case 3: dispatch2<3, OTF>(S, F, x, y, s); break;
+    case 4: dispatch2<4, OTF>(S, F, x, y, s); break;
+    case 5: dispatch2<5, OTF>(S, F, x, y, s); break;
+    case 6: dispatch2<6, OTF>(S, F, x, y, s); break;
+    case 7: dispatch2<7, OTF>(S, F, x, y, s); break;
+    case 8: dispatch2<8, OTF>(S, F, x, y, s); break;
+    case 9: dispatch2<9, OTF>(S, F, x, y, s); break;
+    case 10: dispatch2<10, OTF>(S, F, x, y, s); break;
     default: return false;
   }
   return true;
 }
+
+#ifndef MFWQ_F2_OTF_UNIT
+bool fused2_apply_otf(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s);  // fused2_otf.cu
+
+bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s) {
+  Fused2Plan* F = fused2_plan(S);
+  if (!F->ok) return false;
+  if (S.otf) return fused2_apply_otf(S, *F, x, y, s);
+  return dispatch_p<false>(S, *F, x, y, s);
+}
+#else
+bool fused2_apply_otf(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
+  return dispatch_p<true>(S, F, x, y, s);
+}
+#endif
 
 }  // namespace mfwq

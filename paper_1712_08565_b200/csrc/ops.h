@@ -54,6 +54,15 @@ class Stiffness {
 
   DevBuf<double> pcg_ws;  // PCG work vectors (r, z, p, Ap) + reduction partials, reused across solves
 
+  // on-the-fly coefficients (operators.py:171-183, 207-220): for the analytic maps C depends on
+  // xi1 at most, so the kernel reads C(xi1) from a [6][m1] table instead of 6 N_q grids
+  bool otf = false;
+  DevBuf<double> cx;
+  int geo_kind = 0;
+  double geo_A[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, geo_K[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  bool geo_hasK = false;
+  void set_on_the_fly(int kind, const double* affine9, const double* K9, cudaStream_t s);
+
   // generic-path scratch
   DevBuf<double> g_, t_, s1_, s2_;
   DevBuf<int> flag_;
@@ -100,6 +109,9 @@ struct KrylovOut {
 // device-resident PCG (solvers.py:137-173)
 void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long N, double tol, int maxit,
                std::vector<double>& hist, KrylovOut& out, cudaStream_t s);
+
+// element-blocked fused matvec (fused2.cu); false when the rule is outside its structure
+bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s);
 
 void kron_apply_dense(int d, const int* rows, const int* cols, const double* const* A, const double* x, double* y,
                       int accumulate, cudaStream_t s);

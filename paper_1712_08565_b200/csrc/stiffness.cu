@@ -251,6 +251,8 @@ __global__ void any_nonzero_kernel(const double* __restrict__ C, size_t n, int* 
 
 void Stiffness::set_geometry(int kind, const double* A, const double* K9, const double* J_dev,
                              const double* Kfield_dev, cudaStream_t s) {
+  otf = false;
+  cx.release();
   const size_t G = grid_elems();
   coeff.alloc(6 * G);
   DevBuf<unsigned long long> bad(1);
@@ -286,7 +288,59 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
   detect_nonzero(s);
 }
 
+// On-the-fly mode: C(xi1) = C(xi1, 0, 0) by the same formula as the grids (coeff_kernel); for the
+// identity and affine maps it is constant, for the quarter ring (K = I) it depends on xi1 only
+// (theta drops out of det J J^-1 J^-T; theta = 0 gives the exactly diagonal value).
+void Stiffness::set_on_the_fly(int kind, const double* A, const double* K9, cudaStream_t s) {
+  if (kind != GEOM_IDENTITY && kind != GEOM_AFFINE && kind != GEOM_RING)
+    throw NotImplErr("on-the-fly coefficients need an analytic map (identity, affine or quarter ring)");
+  if (kind == GEOM_RING && K9) {
+    for (int i = 0; i < 9; ++i)
+      if (K9[i] != ((i % 4 == 0) ? 1.0 : 0.0))
+        throw NotImplErr("on-the-fly coefficients on the quarter ring need K = I (C would depend on theta)");
+  }
+  geo_kind = kind;
+  geo_hasK = K9 != nullptr;
+  if (A) std::copy(A, A + 9, geo_A);
+  if (K9) std::copy(K9, K9 + 9, geo_K);
+  const int m1 = dir[0].m;
+  cx.alloc(6 * (size_t)m1);
+  DevBuf<double> zero(1);
+  DevBuf<unsigned long long> bad(1);
+  unsigned long long init = ~0ull;
+  MFWQ_CUDA(cudaMemsetAsync(zero.ptr, 0, sizeof(double), s));
+  MFWQ_CUDA(cudaMemcpyAsync(bad.ptr, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  const double* a = geo_A;
+  const double* k = geo_K;
+  coeff_kernel<<<(m1 + 127) / 128, 128, 0, s>>>(kind, dir[0].pts_d.ptr, zero.ptr, zero.ptr, m1, 1, 1, m1, a[0], a[1],
+                                                a[2], a[3], a[4], a[5], a[6], a[7], a[8], geo_hasK ? 1 : 0, k[0],
+                                                k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], nullptr, nullptr,
+                                                cx.ptr, (size_t)m1, bad.ptr); note_launch();
+  MFWQ_CUDA(cudaGetLastError());
+  std::vector<double> h(6 * (size_t)m1);
+  unsigned long long hbad = 0;
+  MFWQ_CUDA(cudaMemcpyAsync(h.data(), cx.ptr, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  MFWQ_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, sizeof(hbad), cudaMemcpyDeviceToHost, s));
+  MFWQ_CUDA(cudaStreamSynchronize(s));
+  if (hbad != ~0ull) {
+    char msg[160];
+    snprintf(msg, sizeof msg, "non-positive Jacobian determinant at parametric xi1 = %.17g", dir[0].pts[hbad]);
+    throw DegenerateErr(msg);
+  }
+  for (int g = 0; g < 6; ++g) {
+    grid_nonzero[g] = false;
+    for (int q = 0; q < m1; ++q) grid_nonzero[g] = grid_nonzero[g] || h[(size_t)g * m1 + q] != 0.0;
+  }
+  coeff.release();
+  otf = true;
+  coeffs_ready = true;
+  fused_plan.reset();
+  fused2_plan.reset();
+}
+
 void Stiffness::set_coeffs(const double* const* grids, cudaStream_t s) {
+  otf = false;
+  cx.release();
   // grids: 6 device arrays, unpadded (m3, m2, m1) -> repack into the padded layout
   const size_t G = grid_elems();
   coeff.alloc(6 * G);
@@ -419,6 +473,28 @@ void Stiffness::apply_generic(const double* x, double* y, cudaStream_t s) {
 
 void Stiffness::apply(const double* x, double* y, cudaStream_t s) {
   if (!coeffs_ready) throw ValueErr("coefficient grids not set");
+  if (otf) {
+    if (path != 1 && path != 3 && fused2_apply(*this, x, y, s)) return;
+    // the element-blocked kernel cannot take this rule (or a composed path was asked for): evaluate
+    // the grids for this apply only, as the reference's on-the-fly mode does per grid
+    bool nz[6];
+    std::copy(grid_nonzero, grid_nonzero + 6, nz);
+    const double* K9 = geo_hasK ? geo_K : nullptr;
+    DevBuf<double> keep;
+    std::swap(keep.ptr, cx.ptr);
+    std::swap(keep.n, cx.n);
+    set_geometry(geo_kind, geo_A, K9, nullptr, nullptr, s);
+    std::copy(nz, nz + 6, grid_nonzero);
+    if (path == 1) apply_generic(x, y, s);
+    else apply_fused(x, y, s);
+    coeff.release();
+    std::swap(keep.ptr, cx.ptr);
+    std::swap(keep.n, cx.n);
+    otf = true;
+    fused_plan.reset();
+    fused2_plan.reset();
+    return;
+  }
   if (path == 1) { apply_generic(x, y, s); return; }
   apply_fused(x, y, s);
 }

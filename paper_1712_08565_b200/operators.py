@@ -34,13 +34,11 @@ class StiffnessOperator:
     """Matrix-free weighted-quadrature stiffness operator (interior space)."""
 
     def __init__(self, space, rule, geom, K=None, on_the_fly=False, _slab=None):
-        if on_the_fly:
-            raise NotImplementedError("on-the-fly coefficient mode is not built yet (SURVEY 8(f) rank 1)")
         _dev.require_cuda()
         if getattr(space, "dim", 3) != 3 or len(rule.rules) != 3:
             raise NotImplementedError("the B200 operator is three-dimensional")
         self.space, self.rule, self.geom, self.K = space, rule, geom, K
-        self.on_the_fly = False
+        self.on_the_fly = bool(on_the_fly)
         self.d = 3
         self.n_dofs = int(np.prod(space.n_per_dir))
         L = _lib.lib()
@@ -86,13 +84,49 @@ class StiffnessOperator:
             plane = self.n[0] * self.n[1]
             self._in_len = (self.slab["v_hi"] - self.slab["v_lo"]) * plane
             self._out_len = (self.slab["y_hi"] - self.slab["y_lo"]) * plane
-        self._set_geometry(geom, K)
+        if self.on_the_fly:
+            self._set_on_the_fly(geom, K)
+        else:
+            self._set_geometry(geom, K)
+        self._count_flops()
+
+    def _count_flops(self):
+        L = _lib.lib()
         fl = C.c_longlong()
-        _lib.check(L.mfwq_stiffness_flops(h, C.byref(fl)))
-        self.apply_flops = fl.value
-        _lib.check(L.mfwq_stiffness_flops_active(h, C.byref(fl)))
-        self.apply_flops_active = fl.value  # terms with a non-zero grid (what runs)
-        self.setup_flops = COEFF_EVAL_FLOPS * self.n_points * 6
+        _lib.check(L.mfwq_stiffness_flops(self._h, C.byref(fl)))
+        # on the fly, the reference charges one coefficient evaluation per (a, b) and apply
+        # (operators.py:195-198); stored grids are charged once at setup (operators.py:162-163)
+        fly = 9 * COEFF_EVAL_FLOPS * self.n_points if self.on_the_fly else 0
+        self.apply_flops = fl.value + fly
+        _lib.check(L.mfwq_stiffness_flops_active(self._h, C.byref(fl)))
+        self.apply_flops_active = fl.value + fly  # terms with a non-zero coefficient (what runs)
+        self.setup_flops = 0 if self.on_the_fly else COEFF_EVAL_FLOPS * self.n_points * 6
+
+    def _set_on_the_fly(self, geom, K):
+        """Coefficients evaluated inside the kernel from C(xi1) (analytic maps only)."""
+        kind, A = device_kind(geom)
+        if kind == 3:
+            raise NotImplementedError("on-the-fly coefficients need an analytic map (identity, affine or "
+                                      "quarter ring); use stored grids for general geometries")
+        K9 = None
+        if K is not None:
+            Ka = None if callable(K) else np.asarray(K, dtype=float)
+            if Ka is None or Ka.shape != (3, 3):
+                raise NotImplementedError("on-the-fly coefficients take K = None or a constant 3x3 K")
+            K9 = np.ascontiguousarray(Ka)
+        _lib.check(_lib.lib().mfwq_stiffness_set_on_the_fly(
+            self._h, kind, _lib.dptr(A) if A is not None else None, _lib.dptr(K9) if K9 is not None else None,
+            C.c_void_p(_dev.stream_ptr())))
+
+    def set_on_the_fly(self, enabled: bool):
+        """Switch between stored grids and on-the-fly evaluation (operators.py:171-176)."""
+        enabled = bool(enabled)
+        if enabled and not self.on_the_fly:
+            self._set_on_the_fly(self.geom, self.K)
+        elif not enabled and self.on_the_fly:
+            self._set_geometry(self.geom, self.K)
+        self.on_the_fly = enabled
+        self._count_flops()
 
     # -- coefficient grids (operators.py:64-84) --------------------------------
     def _points(self):
@@ -126,11 +160,13 @@ class StiffnessOperator:
 
     @property
     def coeff_scalars(self) -> int:
-        return 6 * self.n_points
+        return 0 if self.on_the_fly else 6 * self.n_points
 
     @property
     def coeffs(self):
-        """The six symmetric grids keyed (a<=b) as host arrays (operators.py:84)."""
+        """The six symmetric grids keyed (a<=b) as host arrays (operators.py:84); None on the fly."""
+        if self.on_the_fly:
+            return None
         out = {}
         for k, key in enumerate(_KEYS):
             g = _dev.empty(self.n_points)

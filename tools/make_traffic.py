@@ -25,5 +25,7 @@ for r in rows[2:]:
     v = lambda k: float(r[col[k]].replace(',', '')) * scale[units[col[k]]]
     per.setdefault(m.group(1), {"dram_bytes": v('dram__bytes_read.sum') + v('dram__bytes_write.sum'),
                                 "ncu_time_us": v('gpu__time_duration.sum')})
-json.dump({"source": src, "per_degree": per}, open(os.path.join(os.path.dirname(__file__), '..', 'profiles', 'traffic.json'), 'w'), indent=1)
+json.dump({"source": src, "per_degree": per,
+           # one sweep step = one launch per degree; comparable with the bench's aggregated algorithmic bytes
+           "bytes_per_launch": sum(v["dram_bytes"] for v in per.values())}, open(os.path.join(os.path.dirname(__file__), '..', 'profiles', 'traffic.json'), 'w'), indent=1)
 print(json.dumps(per, indent=1))

@@ -19,10 +19,11 @@ ap.add_argument("--geom", default="identity")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--fd", type=int, default=0)
 ap.add_argument("--path", default="auto")
+ap.add_argument("--otf", type=int, default=0)
 a = ap.parse_args()
 space = M.tensor_space(a.p, a.n_el)
 A = M.setup_stiffness(space, M.build_tensor_rule(space),
-                      M.identity_map(3) if a.geom == "identity" else M.quarter_ring_map())
+                      M.identity_map(3) if a.geom == "identity" else M.quarter_ring_map(), on_the_fly=bool(a.otf))
 A.set_path(a.path)
 x = torch.from_numpy(np.random.default_rng(0).standard_normal(space.n_dofs)).cuda()
 y = torch.empty_like(x)
