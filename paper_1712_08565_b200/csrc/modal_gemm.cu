@@ -163,8 +163,14 @@ static void launch(const double* A, int lda, int M, int K, const double* X, Mode
 
 void modal_gemm(const double* A, int lda, int M, int K, const double* X, ModeView xv, double* C, ModeView cv,
                 long long N, Scale sc, bool kcontig, cudaStream_t s) {
-  // modes up to 144 wide: one 144-row x 32-col tile (2 x 4 warps of 9 m8 x 1 n8); wider: 128-row tiles
-  if (M <= 144) mg::launch<9, 2, 4, 1>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
+  // modes up to 144 wide: one 144-row x 32-col tile (2 x 4 warps of 9 m8 x 1 n8); wider modes take
+  // 144- or 128-row x 64-col tiles, whichever pads M less (258 = 2 x 144 - 30, not 3 x 128 - 126)
+  if (M <= 144) {
+    mg::launch<9, 2, 4, 1>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
+    return;
+  }
+  const int pad144 = (M + 143) / 144 * 144 - M, pad128 = (M + 127) / 128 * 128 - M;
+  if (pad144 <= pad128) mg::launch<9, 2, 4, 2>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
   else mg::launch<8, 2, 4, 2>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
 }
 
