@@ -520,13 +520,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       const int g2 = sInf->day + r, g1 = sInf->dax + c;
       const size_t plane = (size_t)(i3 - prm.y_lo) * n2;
       if (r < Dy && g2 >= 0 && g2 < n2) {
-#if MFWQ_ABLATE == 4  // timing experiment only: plain stores instead of atomics
-        if (c < Dx && g1 >= 0 && g1 < n1) yv[(plane + g2) * n1 + g1] = d0;
-        if (c + 1 < Dx && g1 + 1 >= 0 && g1 + 1 < n1) yv[(plane + g2) * n1 + g1 + 1] = d1;
-#else
         if (c < Dx && g1 >= 0 && g1 < n1) atomicAdd(&yv[(plane + g2) * n1 + g1], d0);
         if (c + 1 < Dx && g1 + 1 >= 0 && g1 + 1 < n1) atomicAdd(&yv[(plane + g2) * n1 + g1 + 1], d1);
-#endif
       }
     }
     PROF(8)
@@ -635,7 +630,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         push_x(ez);  // ring: planes e3+ez-1 .. e3+ez+p-1, exactly the support of element e3+ez
 #pragma unroll
         for (int pl = 0; pl < 2; ++pl)
-          zpoint(std::true_type{}, 0, 0, 0, sZ + (sQ0[el + ez] - sQ0[el] + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
+          zpoint(std::true_type{}, 0, 0, 0, sZ + (2 * ez + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
         store_row(ez);  // row e3+ez-2 complete
       }
     } else {  // boundary z-elements (extra planes) or the odd tail: C straight from global
