@@ -21,6 +21,7 @@
  *   mfwq_pcg_solve         cg (device-resident loop)                   solvers.py:137-173
  *   mfwq_bicg_*, mfwq_dot2 bicgstab vector updates                     solvers.py:176-249
  *   mfwq_stiffness_set_on_the_fly  on_the_fly=True coefficient mode    operators.py:171-183, 207-220
+ *   mfwq_mass_*            MassOperator / setup_mass                   operators.py:46-61, 87-132
  */
 #ifndef MFWQ_H_
 #define MFWQ_H_
@@ -91,6 +92,17 @@ int mfwq_stiffness_set_geometry(mfwq_stiffness_t h, int kind, const double* affi
    return MFWQ_E_NOTIMPL.  A later set_geometry / set_coeffs returns to stored grids. */
 int mfwq_stiffness_set_on_the_fly(mfwq_stiffness_t h, int kind, const double* affine9, const double* K9,
                                   void* stream);
+/* ---- mass operator (operators.py:46-61, 87-132: MassOperator / setup_mass) ------------------
+   Built on a stiffness handle (same 1D factors): w = (W00 x W00 x W00)(alpha det J o (B0 x B0 x B0) v).
+   alpha: constant, or alpha_field_dev (Nq values of alpha at the mapped points, caller-owned) when
+   non-NULL.  on_the_fly: the alpha det J grid is evaluated per apply instead of stored
+   (operators.py:121-125; analytic maps only).  MFWQ_E_DEGENERATE if det J <= 0.                */
+int mfwq_mass_set(mfwq_stiffness_t h, int kind, const double* affine9, const double* J_dev, double alpha,
+                  const double* alpha_field_dev, int on_the_fly, void* stream);
+/* y = M x (device pointers, length N); y is overwritten */
+int mfwq_mass_apply(mfwq_stiffness_t h, const double* x_dev, double* y_dev, void* stream);
+/* CostMeter count of one mass apply: S(B0) + N_q + S(W00)  (kron.py:90-96, operators.py:118-132) */
+int mfwq_mass_flops(mfwq_stiffness_t h, long long* flops);
 /* six device grids (a<=b order 00,01,02,11,12,22), each (m3,m2,m1) contiguous */
 int mfwq_stiffness_set_coeffs(mfwq_stiffness_t h, const double* const* grids6_dev, void* stream);
 int mfwq_stiffness_get_coeff(mfwq_stiffness_t h, int key, double* out_dev, void* stream);

@@ -10,7 +10,8 @@ from .errors import (DegenerateGeometryError, EigenSolveError,
                      IndefiniteOperatorError, WQConstructionError)
 from .geometry import GeometryMap, affine_map, identity_map, quarter_ring_map
 from .kron import CostMeter, kron_apply, tensor_grid
-from .operators import COEFF_EVAL_FLOPS, StiffnessOperator, setup_stiffness
+from .operators import (COEFF_EVAL_FLOPS, MassOperator, StiffnessOperator, SystemOperator, apply_system,
+                        setup_mass, setup_stiffness)
 from .solvers import (FDPreconditioner, KrylovReport, bicgstab, cg, stopping_tolerance,
                       univariate_parametric_matrices)
 from .splines import (KnotVector, TensorSpace, make_uniform_knots,

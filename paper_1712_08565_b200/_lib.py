@@ -46,6 +46,9 @@ _SIGS = {
     "mfwq_stiffness_set_geometry": (C.c_int, [C.c_void_p, C.c_int, dp, dp, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mfwq_stiffness_set_on_the_fly": (C.c_int, [C.c_void_p, C.c_int, dp, dp, C.c_void_p]),
     "mfwq_stiffness_set_coeffs": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]),
+    "mfwq_mass_set": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_void_p, C.c_double, C.c_void_p, C.c_int, C.c_void_p]),
+    "mfwq_mass_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mfwq_mass_flops": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "mfwq_stiffness_get_coeff": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "mfwq_stiffness_sizes": (C.c_int, [C.c_void_p, ip, ip, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "mfwq_stiffness_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -125,6 +125,23 @@ int mfwq_stiffness_set_on_the_fly(mfwq_stiffness_t h, int kind, const double* af
   });
 }
 
+int mfwq_mass_set(mfwq_stiffness_t h, int kind, const double* affine9, const double* J_dev, double alpha,
+                  const double* alpha_field_dev, int on_the_fly, void* stream) {
+  return guard([&] {
+    if (kind < 0 || kind > 3) throw ValueErr("unknown geometry kind");
+    if (kind == MFWQ_GEOM_JACOBIAN && !J_dev) throw ValueErr("JACOBIAN geometry needs J_dev");
+    h->op.set_mass(kind, affine9, J_dev, alpha, alpha_field_dev, on_the_fly, (cudaStream_t)stream);
+  });
+}
+
+int mfwq_mass_apply(mfwq_stiffness_t h, const double* x, double* y, void* stream) {
+  return guard([&] { h->op.apply_mass(x, y, (cudaStream_t)stream); });
+}
+
+int mfwq_mass_flops(mfwq_stiffness_t h, long long* flops) {
+  return guard([&] { *flops = h->op.mass_flops(); });
+}
+
 int mfwq_stiffness_set_coeffs(mfwq_stiffness_t h, const double* const* grids, void* stream) {
   return guard([&] { h->op.set_coeffs(grids, (cudaStream_t)stream); });
 }

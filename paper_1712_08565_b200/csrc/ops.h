@@ -63,6 +63,18 @@ class Stiffness {
   bool geo_hasK = false;
   void set_on_the_fly(int kind, const double* affine9, const double* K9, cudaStream_t s);
 
+  // mass operator on the same 1D factors (operators.py:87-132): w = (W00 x W00 x W00)(m o (B0 x B0 x B0) v),
+  // m = alpha det J (operators.py:46-61); `mass_grid` (m3, m2, m1p) stored unless on the fly
+  DevBuf<double> mass_grid;
+  bool mass_ready = false, mass_otf = false;
+  double mass_alpha = 1.0;
+  const double* mass_alpha_field = nullptr;  // caller-owned (Nq) alpha values, on-the-fly mode only
+  void set_mass(int kind, const double* affine9, const double* J_dev, double alpha, const double* alpha_field_dev,
+                int on_the_fly, cudaStream_t s);
+  void eval_mass(double* out, const double* J_dev, cudaStream_t s);
+  void apply_mass(const double* x, double* y, cudaStream_t s);
+  long long mass_flops() const;
+
   // generic-path scratch
   DevBuf<double> g_, t_, s1_, s2_;
   DevBuf<int> flag_;

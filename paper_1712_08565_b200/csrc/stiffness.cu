@@ -471,6 +471,119 @@ void Stiffness::apply_generic(const double* x, double* y, cudaStream_t s) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Mass operator (operators.py:46-61, 87-132), composed from the K1 band contractions
+// ---------------------------------------------------------------------------
+__global__ void mass_coeff_kernel(int kind, const double* __restrict__ x1, const double* __restrict__ x2, int m1,
+                                  int m2, int m3, int m1p, double A00, double A01, double A02, double A10, double A11,
+                                  double A12, double A20, double A21, double A22, const double* __restrict__ Jfield,
+                                  double alpha, const double* __restrict__ afield, double* __restrict__ out,
+                                  unsigned long long* bad) {
+  const long long Nq = (long long)m1 * m2 * m3;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Nq; q += (long long)gridDim.x * blockDim.x) {
+    const int q1 = int(q % m1);
+    const long long r = q / m1;
+    const int q2 = int(r % m2);
+    double det;
+    if (kind == GEOM_IDENTITY) {
+      det = 1.0;
+    } else if (kind == GEOM_AFFINE) {
+      det = A00 * (A11 * A22 - A12 * A21) + A01 * (A12 * A20 - A10 * A22) + A02 * (A10 * A21 - A11 * A20);
+    } else if (kind == GEOM_RING) {  // geometry.py:84-94: det J = (pi/2) r (cos^2 + sin^2)
+      const double rr = 1.0 + x1[q1];
+      double sn, cs;
+      sincos(M_PI / 2 * x2[q2], &sn, &cs);
+      det = cs * (M_PI / 2 * rr * cs) + (M_PI / 2 * rr * sn) * sn;
+    } else {
+      const double* J = Jfield + 9 * q;
+      det = J[0] * (J[4] * J[8] - J[5] * J[7]) + J[1] * (J[5] * J[6] - J[3] * J[8]) + J[2] * (J[3] * J[7] - J[4] * J[6]);
+    }
+    if (!(det > 0.0)) atomicMin(bad, (unsigned long long)q);
+    out[(r / m2 * m2 + q2) * (long long)m1p + q1] = (afield ? afield[q] : alpha) * det;
+  }
+}
+
+void Stiffness::set_mass(int kind, const double* A, const double* J_dev, double alpha, const double* afield,
+                         int on_the_fly, cudaStream_t s) {
+  if (is_slab()) throw NotImplErr("the mass operator is not slab-partitioned");
+  if (kind == GEOM_JACOBIAN && on_the_fly) throw NotImplErr("on-the-fly mass needs an analytic map");
+  geo_kind = kind;
+  if (A) std::copy(A, A + 9, geo_A);
+  mass_alpha = alpha;
+  mass_alpha_field = afield;
+  mass_otf = on_the_fly != 0;
+  mass_grid.release();
+  if (!mass_otf) {
+    mass_grid.alloc(grid_elems());
+    eval_mass(mass_grid.ptr, J_dev, s);
+  }
+  mass_ready = true;
+}
+
+void Stiffness::eval_mass(double* out, const double* J_dev, cudaStream_t s) {
+  const int m1 = dir[0].m, m2 = dir[1].m, m3 = dir[2].m;
+  DevBuf<unsigned long long> bad(1);
+  unsigned long long init = ~0ull;
+  MFWQ_CUDA(cudaMemcpyAsync(bad.ptr, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (m1p > m1) MFWQ_CUDA(cudaMemsetAsync(out, 0, grid_elems() * sizeof(double), s));
+  const double* a = geo_A;
+  const int blocks = (int)std::min<long long>((Nq + 255) / 256, 148LL * 16);
+  mass_coeff_kernel<<<blocks, 256, 0, s>>>(geo_kind, dir[0].pts_d.ptr, dir[1].pts_d.ptr, m1, m2, m3, m1p, a[0], a[1],
+                                           a[2], a[3], a[4], a[5], a[6], a[7], a[8], J_dev, mass_alpha,
+                                           mass_alpha_field, out, bad.ptr); note_launch();
+  MFWQ_CUDA(cudaGetLastError());
+  unsigned long long hbad = 0;
+  MFWQ_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, sizeof(hbad), cudaMemcpyDeviceToHost, s));
+  MFWQ_CUDA(cudaStreamSynchronize(s));
+  if (hbad != ~0ull) {
+    const long long q = (long long)hbad;
+    char msg[256];
+    snprintf(msg, sizeof msg, "non-positive Jacobian determinant at parametric point (%.17g, %.17g, %.17g)",
+             dir[0].pts[q % m1], dir[1].pts[(q / m1) % m2], dir[2].pts[q / ((long long)m1 * m2)]);
+    throw DegenerateErr(msg);
+  }
+}
+
+// w = (W00 x W00 x W00)(m o (B0 x B0 x B0) v), contracted direction 3 first (kron.py:83)
+void Stiffness::apply_mass(const double* x, double* y, cudaStream_t s) {
+  if (!mass_ready) throw ValueErr("mass coefficients not set");
+  const int n1 = dir[0].n, n2 = dir[1].n, n3 = dir[2].n;
+  const int m1 = dir[0].m, m2 = dir[1].m, m3 = dir[2].m;
+  if (!g_.ptr) {
+    g_.alloc(Nq);
+    t_.alloc(Nq);
+    s1_.alloc(std::max((long long)m3 * n2 * n1, (long long)n3 * m2 * m1));
+    s2_.alloc(std::max((long long)m3 * m2 * n1, (long long)n3 * n2 * m1));
+  }
+  DevBuf<double> fly;
+  const double* m = mass_grid.ptr;
+  if (mass_otf) {  // operators.py:121-125: evaluated for this apply and dropped
+    fly.alloc(grid_elems());
+    eval_mass(fly.ptr, nullptr, s);
+    m = fly.ptr;
+  }
+  contract(x, s1_.ptr, n1, n2, n3, 2, dir[2].B[0], 0, s);
+  contract(s1_.ptr, s2_.ptr, n1, n2, m3, 1, dir[1].B[0], 0, s);
+  contract(s2_.ptr, g_.ptr, n1, m2, m3, 0, dir[0].B[0], 0, s);
+  const int blocks = (int)std::min<long long>((Nq + 255) / 256, 148LL * 32);
+  scale_kernel<<<blocks, 256, 0, s>>>(m, g_.ptr, t_.ptr, m1, m1p, Nq); note_launch();
+  MFWQ_CUDA(cudaGetLastError());
+  contract(t_.ptr, s1_.ptr, m1, m2, m3, 2, dir[2].W[0], 0, s);
+  contract(s1_.ptr, s2_.ptr, m1, m2, n3, 1, dir[1].W[0], 0, s);
+  contract(s2_.ptr, y, m1, n2, n3, 0, dir[0].W[0], 0, s);
+}
+
+// CostMeter count of one mass apply (operators.py:118-132): S(B0) + N_q + S(W00)
+long long Stiffness::mass_flops() const {
+  const long long n1 = dir[0].n, n2 = dir[1].n, n3 = dir[2].n;
+  const long long m1 = dir[0].m, m2 = dir[1].m, m3 = dir[2].m;
+  auto S = [&](long long z1, long long z2, long long z3, long long s2, long long s3, long long t1, long long t2) {
+    return 2 * z3 * t1 * t2 + 2 * z2 * s3 * t1 + 2 * z1 * s3 * s2;
+  };
+  return S(nnz_[0][0], nnz_[1][0], nnz_[2][0], m2, m3, n1, n2) + Nq +
+         S(nnz_[0][2], nnz_[1][2], nnz_[2][2], n2, n3, m1, m2);
+}
+
 void Stiffness::apply(const double* x, double* y, cudaStream_t s) {
   if (!coeffs_ready) throw ValueErr("coefficient grids not set");
   if (otf) {

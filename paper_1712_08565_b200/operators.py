@@ -30,6 +30,41 @@ def _csr(A):
             np.ascontiguousarray(A.data, dtype=float))
 
 
+def _create_handle(rule, n_dofs):
+    """Library handle holding the rule's 1D factors (operators.py:146-160 restrictions done natively)."""
+    L = _lib.lib()
+    keep = []
+    desc = _lib.StiffnessDesc()
+    for l, r in enumerate(rule.rules):
+        kv = r.kv
+        knots = np.ascontiguousarray(kv.knots, dtype=float)
+        pts = np.ascontiguousarray(r.points, dtype=float)
+        keep += [knots, pts]
+        desc.p[l] = int(kv.degree)
+        desc.nknots[l] = len(knots)
+        desc.knots[l] = _lib.dptr(knots)
+        desc.npts[l] = len(pts)
+        desc.pts[l] = _lib.dptr(pts)
+        mats = [r.weights[(0, 0)], r.weights[(0, 1)], r.weights[(1, 0)], r.weights[(1, 1)],
+                r.colloc[0], r.colloc[1]]
+        for k, M in enumerate(mats):
+            ip, ix, dv = _csr(M)
+            keep += [ip, ix, dv]
+            desc.indptr[6 * l + k] = _lib.iptr(ip)
+            desc.indices[6 * l + k] = _lib.iptr(ix)
+            desc.data[6 * l + k] = _lib.dptr(dv)
+    h = C.c_void_p()
+    _lib.check(L.mfwq_stiffness_create(C.byref(desc), C.byref(h)))
+    n3 = np.zeros(3, np.int32)
+    m3 = np.zeros(3, np.int32)
+    N, Nq = C.c_longlong(), C.c_longlong()
+    _lib.check(L.mfwq_stiffness_sizes(h, _lib.iptr(n3), _lib.iptr(m3), C.byref(N), C.byref(Nq)))
+    if N.value != n_dofs:
+        L.mfwq_stiffness_destroy(h)
+        raise ValueError("rule and space disagree on the number of DoFs")
+    return h, tuple(int(v) for v in n3), tuple(int(v) for v in m3), Nq.value
+
+
 class StiffnessOperator:
     """Matrix-free weighted-quadrature stiffness operator (interior space)."""
 
@@ -37,41 +72,14 @@ class StiffnessOperator:
         _dev.require_cuda()
         if getattr(space, "dim", 3) != 3 or len(rule.rules) != 3:
             raise NotImplementedError("the B200 operator is three-dimensional")
+        self._h = None
         self.space, self.rule, self.geom, self.K = space, rule, geom, K
         self.on_the_fly = bool(on_the_fly)
         self.d = 3
         self.n_dofs = int(np.prod(space.n_per_dir))
         L = _lib.lib()
-        keep = []
-        desc = _lib.StiffnessDesc()
-        for l, r in enumerate(rule.rules):
-            kv = r.kv
-            knots = np.ascontiguousarray(kv.knots, dtype=float)
-            pts = np.ascontiguousarray(r.points, dtype=float)
-            keep += [knots, pts]
-            desc.p[l] = int(kv.degree)
-            desc.nknots[l] = len(knots)
-            desc.knots[l] = _lib.dptr(knots)
-            desc.npts[l] = len(pts)
-            desc.pts[l] = _lib.dptr(pts)
-            mats = [r.weights[(0, 0)], r.weights[(0, 1)], r.weights[(1, 0)], r.weights[(1, 1)],
-                    r.colloc[0], r.colloc[1]]
-            for k, M in enumerate(mats):
-                ip, ix, dv = _csr(M)
-                keep += [ip, ix, dv]
-                desc.indptr[6 * l + k] = _lib.iptr(ip)
-                desc.indices[6 * l + k] = _lib.iptr(ix)
-                desc.data[6 * l + k] = _lib.dptr(dv)
-        h = C.c_void_p()
-        _lib.check(L.mfwq_stiffness_create(C.byref(desc), C.byref(h)))
+        h, self.n, self.m, self.n_points = _create_handle(rule, self.n_dofs)
         self._h = h
-        n3 = np.zeros(3, np.int32)
-        m3 = np.zeros(3, np.int32)
-        N, Nq = C.c_longlong(), C.c_longlong()
-        _lib.check(L.mfwq_stiffness_sizes(h, _lib.iptr(n3), _lib.iptr(m3), C.byref(N), C.byref(Nq)))
-        self.n, self.m, self.n_points = tuple(int(v) for v in n3), tuple(int(v) for v in m3), Nq.value
-        if N.value != self.n_dofs:
-            raise ValueError("rule and space disagree on the number of DoFs")
         # multi-GPU slab of z-elements (paper_1712_08565_b200.dist); None = whole domain
         self.slab = None
         self._in_len = self._out_len = self.n_dofs
@@ -206,3 +214,109 @@ class StiffnessOperator:
 def setup_stiffness(space, rule, geom, K=None, on_the_fly=False) -> StiffnessOperator:
     """operators.py:227-228."""
     return StiffnessOperator(space, rule, geom, K=K, on_the_fly=on_the_fly)
+
+
+class MassOperator:
+    """Matrix-free weighted-quadrature mass operator on the interior space (operators.py:87-132).
+
+    w = (W00 x W00 x W00)(alpha det J o (B0 x B0 x B0) v), composed on the GPU from the banded
+    one-mode contraction kernels; the alpha det J grid is built on the device (operators.py:46-61)
+    or, on the fly, for every apply.
+    """
+
+    def __init__(self, space, rule, geom, alpha=1.0, on_the_fly=False):
+        _dev.require_cuda()
+        if getattr(space, "dim", 3) != 3 or len(rule.rules) != 3:
+            raise NotImplementedError("the B200 operator is three-dimensional")
+        self._h = None
+        self.space, self.rule, self.geom, self.alpha = space, rule, geom, alpha
+        self.on_the_fly = bool(on_the_fly)
+        self.n_dofs = int(np.prod(space.n_per_dir))
+        self.n = tuple(space.n_per_dir)
+        self._h, _, _, self.n_points = _create_handle(rule, self.n_dofs)
+        self._afield = None
+        if callable(alpha):
+            xi = np.stack(tensor_grid([r.points for r in rule.rules]), axis=1)
+            self._afield = _dev.to_device(np.asarray(alpha(geom.evaluate(xi)), dtype=float).reshape(-1),
+                                          self.n_points)[0]
+        self._set(self.on_the_fly)
+
+    def _set(self, fly):
+        kind, A = device_kind(self.geom)
+        J = None
+        if kind == 3:
+            if fly:
+                raise NotImplementedError("on-the-fly mass coefficients need an analytic map")
+            xi = np.stack(tensor_grid([r.points for r in self.rule.rules]), axis=1)
+            J = _dev.to_device(np.asarray(self.geom.jacobian(xi), dtype=float).reshape(-1))[0]
+        a = 1.0 if callable(self.alpha) else float(self.alpha)
+        _lib.check(_lib.lib().mfwq_mass_set(
+            self._h, kind, _lib.dptr(A) if A is not None else None, C.c_void_p(J.data_ptr()) if J is not None else None,
+            a, C.c_void_p(self._afield.data_ptr()) if self._afield is not None else None, int(fly),
+            C.c_void_p(_dev.stream_ptr())))
+        fl = C.c_longlong()
+        _lib.check(_lib.lib().mfwq_mass_flops(self._h, C.byref(fl)))
+        self.apply_flops = fl.value + (COEFF_EVAL_FLOPS * self.n_points if fly else 0)
+        self.setup_flops = 0 if fly else COEFF_EVAL_FLOPS * self.n_points
+
+    @property
+    def coeff_scalars(self) -> int:
+        """Stored coefficient-grid scalars (operators.py:104-107)."""
+        return 0 if self.on_the_fly else self.n_points
+
+    def set_on_the_fly(self, enabled: bool):
+        """Toggle on-the-fly coefficient evaluation (operators.py:109-115)."""
+        enabled = bool(enabled)
+        if enabled != self.on_the_fly:
+            self._set(enabled)
+        self.on_the_fly = enabled
+
+    def apply(self, v, meter: CostMeter | None = None, out=None):
+        x, host = _dev.to_device(v, self.n_dofs)
+        y = out if out is not None else _dev.empty(self.n_dofs)
+        _lib.check(_lib.lib().mfwq_mass_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                              C.c_void_p(_dev.stream_ptr())))
+        if meter is not None:
+            meter.add_flops(self.apply_flops)
+        return _dev.back(y, host)
+
+    __call__ = apply
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.mfwq_stiffness_destroy(h)
+            self._h = None
+
+
+def setup_mass(space, rule, geom, alpha=1.0, on_the_fly=False) -> MassOperator:
+    """operators.py:223-224."""
+    return MassOperator(space, rule, geom, alpha=alpha, on_the_fly=on_the_fly)
+
+
+def apply_system(mass_op, stiff_op, v, meter: CostMeter | None = None):
+    """Stiffness plus mass (operators.py:231-245); the mass term is skipped when absent or alpha == 0."""
+    x, host = _dev.to_device(v, stiff_op.n_dofs)
+    w = stiff_op.apply(x, meter)
+    skip_mass = mass_op is None or (not callable(mass_op.alpha) and float(mass_op.alpha) == 0.0)
+    if not skip_mass:
+        m = mass_op.apply(x, meter)
+        _lib.check(_lib.lib().mfwq_axpy(C.c_void_p(w.data_ptr()), C.c_void_p(m.data_ptr()), w.numel(), 1.0,
+                                        C.c_void_p(_dev.stream_ptr())))
+        if meter is not None:
+            meter.add_flops(2 * stiff_op.n_dofs)
+    return _dev.back(w, host)
+
+
+class SystemOperator:
+    """(stiffness + mass) as a single apply (operators.py:248-257)."""
+
+    def __init__(self, stiff_op, mass_op=None):
+        self.stiff_op = stiff_op
+        self.mass_op = mass_op
+        self.n_dofs = stiff_op.n_dofs
+
+    def apply(self, v, meter: CostMeter | None = None):
+        return apply_system(self.mass_op, self.stiff_op, v, meter)
+
+    __call__ = apply

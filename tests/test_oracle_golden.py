@@ -81,3 +81,28 @@ def test_bicgstab_matches_reference():
         assert np.allclose(hist, ref_hist, rtol=1e-6, atol=1e-12), tag
         xr = z[f"{tag}_x"]
         assert np.linalg.norm(x - xr) <= 1e-9 * max(np.linalg.norm(xr), 1e-300), tag
+
+
+def test_mass_and_system_match_reference():
+    """Oracle mass operator / apply_system (operators.py:46-61, 87-132, 231-245) vs reference runs."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "solvers", "mass_golden.npz"))
+    kv = O.uniform_knots(3, 8)
+    rules = [O.rule_1d(kv)] * 3
+    x = np.random.default_rng(0).standard_normal(O.Stiffness(rules, O.stiffness_coeffs(rules, O.jac_ring)).N)
+    geo = {"ring": (O.jac_ring, O.map_ring), "shear": (O.jac_affine(SHEAR), O.map_affine(SHEAR))}
+    alphas = {"const": 2.5, "field": lambda X: 1.0 + X[:, 0] ** 2 + 0.5 * X[:, 2]}
+    for gname, (jac, fmap) in geo.items():
+        K = O.Stiffness(rules, O.stiffness_coeffs(rules, jac))
+        for aname, alpha in alphas.items():
+            Mo = O.Mass(rules, O.mass_coeff(rules, jac, alpha, fmap))
+            fl = [0]
+            y = Mo.apply(x, fl)
+            ref = z[f"{gname}_{aname}_y"]
+            assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref), (gname, aname)
+            assert fl[0] == int(z[f"{gname}_{aname}_flops"])
+            fl = [0]
+            w = O.apply_system(Mo, K, x, alpha, fl)
+            ref = z[f"{gname}_{aname}_sys"]
+            assert np.linalg.norm(w - ref) <= 1e-13 * np.linalg.norm(ref), (gname, aname)
+            assert fl[0] == int(z[f"{gname}_{aname}_sysflops"])
