@@ -40,7 +40,7 @@
 #if MFWQ_ABLATE == 9  // per-phase cycle counts of one CTA (timing experiment only)
 #define PROF_DECL long long prof_t[10] = {0}; long long prof_last = clock64();
 #define PROF(i) { long long now_ = clock64(); prof_t[i] += now_ - prof_last; prof_last = now_; }
-#define PROF_DUMP if (blockIdx.x == 40 && blockIdx.y == 1 && threadIdx.x == 0) printf("PROF top %lld fetch %lld bdmma %lld bx %lld mbar %lld z %lld sT %lld wx %lld wy %lld plane %lld\n", prof_t[0], prof_t[1], prof_t[2], prof_t[3], prof_t[4], prof_t[5], prof_t[6], prof_t[7], prof_t[8], prof_t[9]);
+#define PROF_DUMP if (blockIdx.x == 40 && blockIdx.y == 0 && (threadIdx.x & 31) == 0) printf("PROF w%d B2wait %lld bside %lld fetch %lld wx %lld mbar %lld z %lld B3wait %lld B4wait %lld wy %lld\n", threadIdx.x >> 5, prof_t[0], prof_t[1], prof_t[2], prof_t[3], prof_t[4], prof_t[5], prof_t[6], prof_t[7], prof_t[8]);
 #else
 #define PROF_DECL
 #define PROF(i)
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 
   const int QE = prm.qe;  // max quadrature planes per z-element
   extern __shared__ __align__(128) double sm[];
-  double* sC = sm + L::oC;       // [ZS*2 planes][G][256]     TMA coefficient stage
+  double* sC = sm + L::oC;       // [G][ZS*2 planes][256]     TMA coefficient stage
   double* sT = sm + L::oT;       // [ZS][NT][16][PK]          emitted W rows (A operand of W x)
   double* sBy = sm + L::oBy;     // [2][16][PKB]              dense By(q2, r)
   double* sWxT = sm + L::oWx;    // [NX][16][PV]              dense Wx^T(ql, c), used x-types
@@ -366,30 +366,23 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   };
   // one stage transaction (thread 0): the z tables of chunk elements [el, el+nz) as one bulk
   // copy of the flat [m3][ZT] table, plus (TMA steps) their coefficient planes -> sC
+  // Warp 0 issues it in parallel: lane 0 arms the barrier, then one lane per copy (the buffers
+  // were only read by the generic proxy since the last fill, and a CTA barrier orders those reads).
   auto issue_stage = [&](int el, int nz) {
-    constexpr int stage = 0;
-    if (tid == 0) {
-      // order the previous step's generic-proxy reads of sC / sZ before the async overwrite
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      const bool tma = !OTF && nz == ZS && sStep[el / ZS];
-      const int qa = sQ0[el];
-      const unsigned zbytes = (unsigned)((sQ0[el + nz] - qa) * ZT * 8);
-      mbar_expect_tx(&mbar[stage], zbytes + (tma ? ZS * G * 2 * TQ * TQ * 8 : 0));
-      bulk_load(sZ, prm.ztab + (size_t)qa * ZT, zbytes, &mbar[stage]);
-      if (!tma) return;
+    if (warp != 0) return;
+    const bool tma = !OTF && nz == ZS && sStep[el / ZS];
+    const int qa = sQ0[el];
+    const unsigned zbytes = (unsigned)((sQ0[el + nz] - qa) * ZT * 8);
+    if (lane == 0) mbar_expect_tx(&mbar[0], zbytes + (tma ? ZS * G * 2 * TQ * TQ * 8 : 0));
+    __syncwarp();
+    if (lane == 0) bulk_load(sZ, prm.ztab + (size_t)qa * ZT, zbytes, &mbar[0]);
+    static_assert(ZS == 2, "one 16 x 16 x 4 box per grid covers the step's planes");
+    if (tma && lane == 0) {  // regular step: planes sQ0[el] .. +3 are contiguous -> sC [grid][plane][256]
 #pragma unroll
-      for (int ez = 0; ez < ZS; ++ez) {
-        const int qa = sQ0[el + ez];
-#pragma unroll
-        for (int g = 0; g < 6; ++g) {
-          if (!grid_used<NT>(g)) continue;
-          const int sl = grid_slot<NT>(g);
-#pragma unroll
-          for (int pl = 0; pl < 2; ++pl)
-            tma_load_3d(sC + ((ez * 2 + pl) * G + sl) * 256, &maps.m[g], sInf->q0x, sInf->q0y,
-                        qa + pl - prm.qzb, &mbar[stage]);
-        }
-      }
+      for (int g = 0; g < 6; ++g)
+        if (grid_used<NT>(g))
+          tma_load_3d(sC + grid_slot<NT>(g) * (2 * ZS) * 256, &maps.m[g], sInf->q0x, sInf->q0y, qa - prm.qzb,
+                      &mbar[0]);
     }
   };
   // a step takes its coefficients by TMA when it has ZS elements of exactly 2 planes each
@@ -556,7 +549,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     for (int g = 0; g < 6; ++g) {
       if (!grid_used<NT>(g)) { cg[g] = 0.0; continue; }
       if constexpr (OTF) cg[g] = active ? sCx[grid_slot<NT>(g) * TQ + ql1] : 0.0;
-      else if constexpr (kTMA) cg[g] = active ? cst[grid_slot<NT>(g) * 256] : 0.0;
+      else if constexpr (kTMA) cg[g] = active ? cst[grid_slot<NT>(g) * (2 * ZS) * 256] : 0.0;
       else cg[g] = active ? __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * prm.m[1] + sInf->q0y + ql2) * prm.m1p + sInf->q0x + ql1) : 0.0;
     }
     double tv[NT];
@@ -620,6 +613,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     if (eln < nez)
       for (int z = 0; z < nzn; ++z) fetch_plane(e3 + nz + P - 1 + z, z);  // next step's planes
     cp_commit();
+    PROF(2)
     mbar_wait(&mbar[0], parity);  // z rows (and TMA coefficient planes) landed
     parity ^= 1u;
     PROF(4)
@@ -630,7 +624,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         push_x(ez);  // ring: planes e3+ez-1 .. e3+ez+p-1, exactly the support of element e3+ez
 #pragma unroll
         for (int pl = 0; pl < 2; ++pl)
-          zpoint(std::true_type{}, 0, 0, 0, sZ + (2 * ez + pl) * ZT, cst + (ez * 2 + pl) * G * 256);
+          zpoint(std::true_type{}, 0, 0, 0, sZ + (2 * ez + pl) * ZT, cst + (ez * 2 + pl) * 256);
         store_row(ez);  // row e3+ez-2 complete
       }
     } else {  // boundary z-elements (extra planes) or the odd tail: C straight from global
@@ -650,6 +644,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     if (eln < nez) issue_stage(eln, nzn);
     const bool rv = rows_valid(nz, e3 - 2);
     if (rv) w_x(std::integral_constant<int, nz>{});
+    PROF(3)
     __syncthreads();  // B4: sS complete
     PROF(7)
     if (rv) w_y(std::integral_constant<int, nz>{}, e3 - 2);
@@ -657,6 +652,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       if (nzn == ZS) bside_y(ZS);
       else bside_y(1);
     }
+    PROF(1)
   };
 
   int el = 0;
@@ -851,7 +847,7 @@ void encode_maps(Stiffness& S, Fused2Plan& F) {
   for (int g = 0; g < 6; ++g) {
     cuuint64_t dims[3] = {(cuuint64_t)S.dir[0].m, (cuuint64_t)S.dir[1].m, (cuuint64_t)(S.q_hi - S.q_lo)};
     cuuint64_t strides[2] = {(cuuint64_t)S.m1p * 8, (cuuint64_t)S.m1p * S.dir[1].m * 8};
-    cuuint32_t box[3] = {(cuuint32_t)f2::TQ, (cuuint32_t)f2::TQ, 1};
+    cuuint32_t box[3] = {(cuuint32_t)f2::TQ, (cuuint32_t)f2::TQ, 4};  // the 2 x 2 planes of a regular step
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(&F.maps.m[g], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(S.coeff.ptr + g * G), dims,
                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
