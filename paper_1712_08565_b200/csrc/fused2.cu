@@ -368,21 +368,28 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   // copy of the flat [m3][ZT] table, plus (TMA steps) their coefficient planes -> sC
   // Warp 0 issues it in parallel: lane 0 arms the barrier, then one lane per copy (the buffers
   // were only read by the generic proxy since the last fill, and a CTA barrier orders those reads).
-  auto issue_stage = [&](int el, int nz) {
-    if (warp != 0) return;
+  // arm_stage (thread 0, once the previous phase has completed) sets the transaction bytes;
+  // issue_stage (after the barrier that frees sC / sZ) spreads the copies over warps 0..G, lane 0
+  // each: warp 0 the bulk z rows, warp 1 + slot one 16 x 16 x 4 coefficient box per used grid
+  static_assert(ZS == 2, "one 16 x 16 x 4 box per grid covers a regular step's 2 x 2 planes");
+  auto arm_stage = [&](int el, int nz) {
+    if (tid != 0) return;
     const bool tma = !OTF && nz == ZS && sStep[el / ZS];
+    const unsigned zbytes = (unsigned)((sQ0[el + nz] - sQ0[el]) * ZT * 8);
+    mbar_expect_tx(&mbar[0], zbytes + (tma ? ZS * G * 2 * TQ * TQ * 8 : 0));
+  };
+  auto issue_stage = [&](int el, int nz) {
+    if (lane != 0 || warp > G) return;
     const int qa = sQ0[el];
-    const unsigned zbytes = (unsigned)((sQ0[el + nz] - qa) * ZT * 8);
-    if (lane == 0) mbar_expect_tx(&mbar[0], zbytes + (tma ? ZS * G * 2 * TQ * TQ * 8 : 0));
-    __syncwarp();
-    if (lane == 0) bulk_load(sZ, prm.ztab + (size_t)qa * ZT, zbytes, &mbar[0]);
-    static_assert(ZS == 2, "one 16 x 16 x 4 box per grid covers the step's planes");
-    if (tma && lane == 0) {  // regular step: planes sQ0[el] .. +3 are contiguous -> sC [grid][plane][256]
+    if (warp == 0) {
+      bulk_load(sZ, prm.ztab + (size_t)qa * ZT, (unsigned)((sQ0[el + nz] - qa) * ZT * 8), &mbar[0]);
+    } else if (!OTF && nz == ZS && sStep[el / ZS]) {  // regular step: planes qa .. qa+3 -> sC [slot][plane][256]
+      const int sl = warp - 1;
+      int g = 0;
 #pragma unroll
-      for (int g = 0; g < 6; ++g)
-        if (grid_used<NT>(g))
-          tma_load_3d(sC + grid_slot<NT>(g) * (2 * ZS) * 256, &maps.m[g], sInf->q0x, sInf->q0y, qa - prm.qzb,
-                      &mbar[0]);
+      for (int h = 0; h < 6; ++h)
+        if (grid_used<NT>(h) && grid_slot<NT>(h) == sl) g = h;
+      tma_load_3d(sC + sl * (2 * ZS) * 256, &maps.m[g], sInf->q0x, sInf->q0y, qa - prm.qzb, &mbar[0]);
     }
   };
   // a step takes its coefficients by TMA when it has ZS elements of exactly 2 planes each
@@ -594,6 +601,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     const int nz0 = nez >= ZS ? ZS : 1;
     for (int z = 0; z < nz0; ++z) fetch_plane(tz.ea + P - 1 + z, z);
     cp_commit();
+    arm_stage(0, nz0);
+    __syncthreads();  // armed before any copy of the phase lands
     issue_stage(0, nz0);
     cp_wait_all();
     __syncthreads();
@@ -638,6 +647,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       }
     }
     PROF(5)
+    if (eln < nez) arm_stage(eln, nzn);  // next phase (this one completed above); copies follow B3
     cp_wait_all();
     __syncthreads();  // B3: sT complete, all reads of sC / sZ done, next v planes landed
     PROF(6)
