@@ -52,8 +52,9 @@ __global__ void __launch_bounds__(WM * WN * 32, 2)
   double* Bs = sm + STAGES * BM * PA;       // [STAGES][BK][PB]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WN, wn = warp % WN;
-  const long long n0 = (long long)blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
+  // M tiles of one N block are adjacent in launch order, so they share the X tile in L2
+  const long long n0 = (long long)blockIdx.y * BN;
+  const int m0 = blockIdx.x * BM;
 
   // the B-tile columns a thread loads are the same for every k-tile: precompute their offsets
   constexpr int BPER = (BK * BN) / THREADS;
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(WM * WN * 32, 2)
     const double* bs = Bs + (kt % STAGES) * BK * PB + (lane & 3) * PB + wn * NTW * 8 + (lane >> 2);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
+      if (kt == nk - 1 && kt * BK + kk >= K) break;  // zero-padded k-steps of the last tile (warp-uniform)
       double b[NTW];
 #pragma unroll
       for (int j = 0; j < NTW; ++j) b[j] = bs[kk * PB + j * 8];
@@ -146,7 +148,7 @@ static void launch(const double* A, int lda, int M, int K, const double* X, Mode
                    long long N, Scale sc, bool kc, cudaStream_t s) {
   constexpr int BM = 8 * MT * WM, THREADS = WM * WN * 32, BN = WN * NTW * 8;
   const size_t smem = sizeof(double) * STAGES * (BM * (BK + APAD) + BK * (BN + BPAD));
-  dim3 grid((unsigned)((N + BN - 1) / BN), (M + BM - 1) / BM);
+  dim3 grid((M + BM - 1) / BM, (unsigned)((N + BN - 1) / BN));
   if (kc) {
     auto k = modal_kernel<MT, WM, WN, NTW, true>;
     MFWQ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -163,14 +165,20 @@ static void launch(const double* A, int lda, int M, int K, const double* X, Mode
 
 void modal_gemm(const double* A, int lda, int M, int K, const double* X, ModeView xv, double* C, ModeView cv,
                 long long N, Scale sc, bool kcontig, cudaStream_t s) {
-  // modes up to 144 wide: one 144-row x 32-col tile (2 x 4 warps of 9 m8 x 1 n8); wider modes take
-  // 144- or 128-row x 64-col tiles, whichever pads M less (258 = 2 x 144 - 30, not 3 x 128 - 126)
+  // one mode <= 144 wide: a single 128- or 144-row x 32-col tile (2 x 4 warps of 8 or 9 m8 x 1 n8);
+  // wider modes: the row tiling (144, 128 or 88 rows) that pads M least, e.g. 258 = 3 x 88 - 6
+  if (M <= 128) {
+    mg::launch<8, 2, 4, 1>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
+    return;
+  }
   if (M <= 144) {
     mg::launch<9, 2, 4, 1>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
     return;
   }
-  const int pad144 = (M + 143) / 144 * 144 - M, pad128 = (M + 127) / 128 * 128 - M;
-  if (pad144 <= pad128) mg::launch<9, 2, 4, 2>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
+  auto pad = [&](int bm) { return (M + bm - 1) / bm * bm - M; };
+  const int p144 = pad(144), p128 = pad(128), p88 = pad(88);
+  if (p88 < p144 && p88 < p128) mg::launch<11, 1, 8, 2>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
+  else if (p144 <= p128) mg::launch<9, 2, 4, 2>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
   else mg::launch<8, 2, 4, 2>(A, lda, M, K, X, xv, C, cv, N, sc, kcontig, s);
 }
 
