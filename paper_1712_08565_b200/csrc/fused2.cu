@@ -37,6 +37,9 @@
 #ifndef MFWQ_ABLATE
 #define MFWQ_ABLATE 0  // timing experiments only (tools/ablate.sh); 0 in every product build
 #endif
+#ifndef MFWQ_ABL_MASK
+#define MFWQ_ABL_MASK 0  // timing experiments only: 1 bside_y, 2 z-part, 4 w_x, 8 w_y, 16 fetch, 32 push_x off
+#endif
 #if MFWQ_ABLATE == 9  // per-phase cycle counts of one CTA (timing experiment only)
 #define PROF_DECL long long prof_t[10] = {0}; long long prof_last = clock64();
 #define PROF(i) { long long now_ = clock64(); prof_t[i] += now_ - prof_last; prof_last = now_; }
@@ -54,6 +57,11 @@ constexpr int TQ = 16, NTHR = 256, NWARP = 8;
 constexpr int PV = 24;   // pitch (doubles) of N-operand tiles (V, Wx^T, S, A): 24 = 8 mod 16 -> conflict-free B frags
 constexpr int PK = 20;   // pitch of K-major A-operand tiles with K <= 16 (T, Wy)
 constexpr int PKB = 28;  // pitch of By (K = window rows, up to 24)
+// B-fragment tiles (read as [k = lane&3][n = lane>>2], pitch PV) are XOR-swizzled: element (r, c) sits
+// at r*PV + (c ^ swz(r)).  With PV = 8 mod 16, rows k and k+2 would share banks inside a half-warp;
+// flipping column bit 2 on rows with bit 1 set makes the 16 lanes of each half hit 16 distinct
+// 8-byte slots, and keeps the double2 pairs of C-fragment stores adjacent.
+__host__ __device__ constexpr int swz(int r) { return (r & 2) << 1; }
 
 struct Tile {
   int ea, eb;  // elements [ea, eb)
@@ -91,6 +99,7 @@ struct Params {
   const double* cx;  // on-the-fly mode: C_g(xi1) table [6][m1]
 };
 
+
 struct Maps {
   CUtensorMap m[6];  // per coefficient grid, 16 x 16 x 1 boxes (zero fill past the grid edge)
 };
@@ -124,6 +133,12 @@ __host__ __device__ constexpr int grid_slot(int g) {  // position of grid g amon
   int n = 0;
   for (int h = 0; h < g; ++h) n += grid_used<NT>(h) ? 1 : 0;
   return n;
+}
+template <int NT>
+__host__ __device__ constexpr bool ztype_used(int w) {
+  bool u = false;
+  for (int t = 0; t < NT; ++t) u = u || wtype(Terms<NT>::a(t), Terms<NT>::b(t), 2) == w;
+  return u;
 }
 template <int NT>
 __host__ __device__ constexpr bool ytype_used(int w) {
@@ -276,7 +291,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sEy + TQ);
   // tile scalars live in shared memory (re-read after each barrier) instead of pinning
   // registers across the whole z loop
-  struct TileInfo { int Dx, Dy, dax, day, nez, ea3, q0x, q0y; };
+  struct TileInfo { int Dx, Dy, dax, day, nez, ea3, q0x, q0y, pend_nz, pend_i3; };
   TileInfo* sInf = reinterpret_cast<TileInfo*>(mbar + 2);
   int* sQ0 = reinterpret_cast<int*>(sInf + 1);
 
@@ -311,7 +326,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     }
     for (int i = tid; i <= nez; i += NTHR) sQ0[i] = prm.q0z[tz.ea + i];
     if (tid == 0) {
-      *sInf = TileInfo{Dx, Dy, dax, day, nez, tz.ea, tx.q0, ty.q0};
+      *sInf = TileInfo{Dx, Dy, dax, day, nez, tz.ea, tx.q0, ty.q0, 0, 0};
       mbar_init(&mbar[0], 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
@@ -351,10 +366,10 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   for (int k = 0; k < FPT; ++k) {
     const int e = tid + k * NTHR, r = e / Dx, c = e % Dx, g2 = day + r, g1 = dax + c;
     const bool ok = e < Dy * Dx && g2 >= 0 && g2 < n2 && g1 >= 0 && g1 < n1;
-    sFP[k * NTHR + tid] = ok ? ((g2 * n1 + g1) << 10) | (r * PV + c) : -1;
+    sFP[k * NTHR + tid] = ok ? ((g2 * n1 + g1) << 10) | (r * PV + (c ^ swz(r))) : -1;
   }
   auto fetch_plane = [&](int i3, int z) {
-    if (MFWQ_ABLATE == 5) return;
+    if (MFWQ_ABLATE == 5 || (MFWQ_ABL_MASK & 16)) return;
     const bool vp = i3 >= prm.v_lo && i3 < prm.v_hi;
     double* dst = sV + z * VR * PV;
     const double* src = xv + (vp ? (size_t)(i3 - prm.v_lo) * prm.n2 * prm.n1 : 0);
@@ -401,6 +416,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 
   // push one DoF plane (already contracted in y into sA[z]) through the x-contraction into the ring
   auto push_x = [&](int z) {
+    if (MFWQ_ABL_MASK & 32) return;
     double vx = 0.0, vy = 0.0, v0 = 0.0;
     const double* a0 = sA + (z * 2 * TQ + ql2) * PV + ex + 1;
     const double* a1 = a0 + TQ * PV;
@@ -425,7 +441,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   };
   // B side, in-plane: DMMA y-contraction of nz planes of sV -> sA
   auto bside_y = [&](int nz) {
-    for (int task = warp; task < (MFWQ_ABLATE == 2 ? 0 : 2 * 2 * NTD); task += NWARP) {  // (b, mt, nt)
+    for (int task = warp; task < ((MFWQ_ABLATE == 2 || (MFWQ_ABL_MASK & 1)) ? 0 : 2 * 2 * NTD); task += NWARP) {  // (b, mt, nt)
       const int b = task / (2 * NTD), mt = (task / NTD) % 2, nt = task % NTD;
       const double* ap = sBy + (b * TQ + mt * 8 + (lane >> 2)) * PKB + (lane & 3);
       double a[KB];
@@ -434,7 +450,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #pragma unroll
       for (int z = 0; z < ZS; ++z) {
         if (z >= nz) break;
-        const double* bp = sV + z * VR * PV + (lane & 3) * PV + nt * 8 + (lane >> 2);
+        const double* bp = sV + z * VR * PV + (lane & 3) * PV + ((nt * 8 + (lane >> 2)) ^ swz(lane & 3));
         double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KB; ks += 2) {
@@ -481,13 +497,13 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
           if (yslot<NT>(wtype(T::a(t), T::b(t), 1)) != ys) continue;  // warp-uniform
           const int xs = xslot<NT>(wtype(T::a(t), T::b(t), 0));
           const double* ap = sT + ((z * NT + t) * TQ + mt * 8 + (lane >> 2)) * PK + (lane & 3);
-          const double* bp = sWxT + (xs * TQ + (lane & 3)) * PV + nt * 8 + (lane >> 2);
+          const double* bp = sWxT + (xs * TQ + (lane & 3)) * PV + ((nt * 8 + (lane >> 2)) ^ swz(lane & 3));
           dmma(d0, d1, ap[0], bp[0]);
           dmma(e0, e1, ap[4], bp[4 * PV]);
           dmma(d0, d1, ap[8], bp[8 * PV]);
           dmma(e0, e1, ap[12], bp[12 * PV]);
         }
-        double* o = sS + ((z * NY + ys) * TQ + mt * 8 + (lane >> 2)) * PV + nt * 8 + 2 * (lane & 3);
+        double* o = sS + ((z * NY + ys) * TQ + mt * 8 + (lane >> 2)) * PV + ((nt * 8 + 2 * (lane & 3)) ^ swz(lane >> 2));
         *reinterpret_cast<double2*>(o) = make_double2(d0 + e0, d1 + e1);
       }
     }
@@ -508,7 +524,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         for (int ks = 0; ks < 4; ++ks) {
           const int kq = ks * 4 + (lane & 3);
           const double a = sWy[(yslot<NT>(w) * PV + mt * 8 + (lane >> 2)) * PK + kq];
-          const double bb = sS[((z * L::NY + yslot<NT>(w)) * TQ + kq) * PV + nt * 8 + (lane >> 2)];
+          const double bb = sS[((z * L::NY + yslot<NT>(w)) * TQ + kq) * PV + ((nt * 8 + (lane >> 2)) ^ swz(lane & 3))];
           if (chain++ & 1) dmma(e0, e1, a, bb);
           else dmma(d0, d1, a, bb);
         }
@@ -519,6 +535,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       const int n1 = prm.n1, n2 = prm.n2, Dx = sInf->Dx, Dy = sInf->Dy;
       const int g2 = sInf->day + r, g1 = sInf->dax + c;
       const size_t plane = (size_t)(i3 - prm.y_lo) * n2;
+      if (MFWQ_ABLATE == 14 && d0 != 1234.5) continue;
       if (r < Dy && g2 >= 0 && g2 < n2) {
         if (c < Dx && g1 >= 0 && g1 < n1) atomicAdd(&yv[(plane + g2) * n1 + g1], d0);
         if (c + 1 < Dx && g1 + 1 >= 0 && g1 + 1 < n1) atomicAdd(&yv[(plane + g2) * n1 + g1 + 1], d1);
@@ -586,6 +603,65 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   };
   const int cthr = ql2 * TQ + ql1;  // this thread's point inside a TMA coefficient box
 
+  // Regular element (exactly two quadrature planes, coefficients in the TMA stage): the z-part of
+  // both planes interleaved, so each thread keeps six independent gradient chains and then
+  // eighteen-odd two-deep accumulator chains in flight instead of one plane's dependent sequence.
+  // zr: the plane-0 row of the z table (plane 1 follows at zs doubles).
+  auto zelem = [&](const double* zr, int zs, const double* cst) {
+    double g[2][3];
+#pragma unroll
+    for (int pl = 0; pl < 2; ++pl) g[pl][0] = g[pl][1] = g[pl][2] = 0.0;
+#pragma unroll
+    for (int k2 = 0; k2 < NBP / 2; ++k2)
+#pragma unroll
+      for (int pl = 0; pl < 2; ++pl) {
+        const double2 c0 = reinterpret_cast<const double2*>(zr + pl * zs)[k2];
+        const double2 c1 = reinterpret_cast<const double2*>(zr + pl * zs + NBP)[k2];
+        const int k = 2 * k2;
+        g[pl][0] = fma(c0.x, hx[k], g[pl][0]);
+        g[pl][1] = fma(c0.x, hy[k], g[pl][1]);
+        g[pl][2] = fma(c1.x, h0[k], g[pl][2]);
+        if (k + 1 < NB) {
+          g[pl][0] = fma(c0.y, hx[k + 1], g[pl][0]);
+          g[pl][1] = fma(c0.y, hy[k + 1], g[pl][1]);
+          g[pl][2] = fma(c1.y, h0[k + 1], g[pl][2]);
+        }
+      }
+    double tv[2][NT];
+#pragma unroll
+    for (int pl = 0; pl < 2; ++pl) {
+      double cg[6];
+#pragma unroll
+      for (int gg = 0; gg < 6; ++gg) {
+        if (!grid_used<NT>(gg)) { cg[gg] = 0.0; continue; }
+        if constexpr (OTF) cg[gg] = active ? sCx[grid_slot<NT>(gg) * TQ + ql1] : 0.0;
+        else cg[gg] = active ? cst[pl * 256 + grid_slot<NT>(gg) * (2 * ZS) * 256] : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int b = T::b(t);
+        tv[pl][t] = cg[gkey(T::a(t), b)] * g[pl][b];
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      if (!ztype_used<NT>(w)) continue;
+      const double* w0 = zr + 2 * NBP + w * NWP;
+#pragma unroll
+      for (int k2 = 0; k2 < NWP / 2; ++k2) {
+        const double2 c0 = reinterpret_cast<const double2*>(w0)[k2];
+        const double2 c1 = reinterpret_cast<const double2*>(w0 + zs)[k2];
+        const int k = 2 * k2;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (wtype(T::a(t), T::b(t), 2) != w) continue;
+          acc[t][k] = fma(c1.x, tv[1][t], fma(c0.x, tv[0][t], acc[t][k]));
+          if (k + 1 < NW) acc[t][k + 1] = fma(c1.y, tv[1][t], fma(c0.y, tv[0][t], acc[t][k + 1]));
+        }
+      }
+    }
+  };
+
   // ---- prologue: fill the ring with planes ea-1 .. ea+p-2 ----------------------
   for (int k = 0; k < P; ++k) {
     fetch_plane(tz.ea - 1 + k, 0);
@@ -612,17 +688,27 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 
   // One step over NZ (compile-time) z-elements starting at chunk element el. Phases between the
   // three barriers:  [B2] next v planes, z-part  [B3] next stage, W x  [B4] W y || next B-side y
+  // Two CTA barriers per step:  [B2] next v planes, W y of the previous step, z-part
+  // [B3] next stage, W x, next B-side y.  (w_y(k-1) | z(k) and w_x(k) | bside_y(k+1) are independent.)
   auto do_step = [&](auto NZc, int el) {
     constexpr int nz = decltype(NZc)::value;
     const int e3 = sInf->ea3 + el, nez = sInf->nez;
     const int eln = el + nz;
     const int nzn = (nez - eln) >= ZS ? ZS : 1;
-    __syncthreads();  // B2: sA of this step complete, sV free
+    __syncthreads();  // B2: sA of this step and sS of the previous one complete, sV / sT free
     PROF(0)
     if (eln < nez)
       for (int z = 0; z < nzn; ++z) fetch_plane(e3 + nz + P - 1 + z, z);  // next step's planes
     cp_commit();
     PROF(2)
+    // the previous step's W y-contraction (DMMA + atomics) shares this phase with the z-part:
+    // independent work, and the stage copies get longer to land
+    if (MFWQ_ABLATE != 12 && !(MFWQ_ABL_MASK & 8)) {
+      const int pend_nz = sInf->pend_nz;
+      if (pend_nz == 2) w_y(std::integral_constant<int, 2>{}, sInf->pend_i3);
+      else if (pend_nz == 1) w_y(std::integral_constant<int, 1>{}, sInf->pend_i3);
+    }
+    PROF(7)
     mbar_wait(&mbar[0], parity);  // z rows (and TMA coefficient planes) landed
     parity ^= 1u;
     PROF(4)
@@ -631,9 +717,14 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
 #pragma unroll
       for (int ez = 0; ez < nz; ++ez) {
         push_x(ez);  // ring: planes e3+ez-1 .. e3+ez+p-1, exactly the support of element e3+ez
+        if (MFWQ_ABLATE == 13 || (MFWQ_ABL_MASK & 2)) {
+        } else if constexpr (P <= 4) {
+          zelem(sZ + 2 * ez * ZT, ZT, cst + ez * 2 * 256);
+        } else {  // high degree: one plane at a time keeps the live state inside 128 registers
 #pragma unroll
-        for (int pl = 0; pl < 2; ++pl)
-          zpoint(std::true_type{}, 0, 0, 0, sZ + (2 * ez + pl) * ZT, cst + (ez * 2 + pl) * 256);
+          for (int pl = 0; pl < 2; ++pl)
+            zpoint(std::true_type{}, 0, 0, 0, sZ + (2 * ez + pl) * ZT, cst + (ez * 2 + pl) * 256);
+        }
         store_row(ez);  // row e3+ez-2 complete
       }
     } else {  // boundary z-elements (extra planes) or the odd tail: C straight from global
@@ -653,11 +744,12 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     PROF(6)
     if (eln < nez) issue_stage(eln, nzn);
     const bool rv = rows_valid(nz, e3 - 2);
-    if (rv) w_x(std::integral_constant<int, nz>{});
+    if (rv && MFWQ_ABLATE != 11 && !(MFWQ_ABL_MASK & 4)) w_x(std::integral_constant<int, nz>{});
     PROF(3)
-    __syncthreads();  // B4: sS complete
-    PROF(7)
-    if (rv) w_y(std::integral_constant<int, nz>{}, e3 - 2);
+    if (tid == 0) {  // its W y runs in the next z phase (or after the loop); read after the next barrier
+      sInf->pend_nz = rv ? nz : 0;
+      sInf->pend_i3 = e3 - 2;
+    }
     if (eln < nez) {
       if (nzn == ZS) bside_y(ZS);
       else bside_y(1);
@@ -668,6 +760,9 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   int el = 0;
   for (; el + ZS <= sInf->nez; el += ZS) do_step(std::integral_constant<int, ZS>{}, el);
   if (el < sInf->nez) do_step(std::integral_constant<int, 1>{}, el);  // odd tail
+  __syncthreads();  // sS of the last step complete, its W x done with sT
+  if (sInf->pend_nz == 2) w_y(std::integral_constant<int, 2>{}, sInf->pend_i3);
+  else if (sInf->pend_nz == 1) w_y(std::integral_constant<int, 1>{}, sInf->pend_i3);
   // flush the open planes (partial; neighbours add theirs): slot k holds interior row eb-2+k
   for (int k = 0; k < NW - 1; ++k) {
     const int i3 = sInf->ea3 + sInf->nez - 2 + k;
@@ -697,7 +792,7 @@ struct Fused2Plan {
   int ntile[3] = {0, 0, 0};
   int max_nqz = 0, qe = 0, max_chunk = 0;
   const double* maps_for = nullptr;  // coefficient buffer the maps were encoded for
-  f2::Maps maps;
+  f2::Maps maps;  // 16 x 16 x 4 boxes: the 2 x 2 planes of a regular step
 };
 
 bool build_elem_tables(const Dir1D& d, std::vector<double>& B, std::vector<double>& W, std::vector<int>& eq);
@@ -796,7 +891,7 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
         for (int w = 0; w < 4; ++w)  // Wx^T(ql, c) = Wt[w][ql][c - e(ql)]
           for (int c = 0; c < PV; ++c) {
             const int k = c - ex;
-            if (k >= 0 && k < NW) o[(w * TQ + q) * PV + c] = HW[0][((size_t)w * m1 + t.q0 + q) * NW + k];
+            if (k >= 0 && k < NW) o[(w * TQ + q) * PV + (c ^ swz(q))] = HW[0][((size_t)w * m1 + t.q0 + q) * NW + k];
           }
         for (int b = 0; b < 2; ++b)
           for (int k = 0; k < NB; ++k) o[4 * TQ * PV + (b * TQ + q) * NB + k] = HB[0][((size_t)b * m1 + t.q0 + q) * NB + k];
