@@ -19,7 +19,7 @@ col = {h: i for i, h in enumerate(hdr)}
 scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1, 'us': 1, 'msecond': 1e3, 'ms': 1e3}
 per = {}
 for r in rows[2:]:
-    m = re.search(r'k_fused<(\d+), (\d+), (\d+)>', r[col['Kernel Name']])
+    m = re.search(r'k_fused<(\d+), (\d+), (\d+), (?:0|false)>', r[col['Kernel Name']])
     if not m:
         continue
     v = lambda k: float(r[col[k]].replace(',', '')) * scale[units[col[k]]]
