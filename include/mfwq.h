@@ -125,6 +125,36 @@ int mfwq_stiffness_flops(mfwq_stiffness_t h, long long* flops);
 int mfwq_stiffness_flops_active(mfwq_stiffness_t h, long long* flops);
 void mfwq_stiffness_destroy(mfwq_stiffness_t h);
 
+/* ---------------- tensor-Gauss quadrature: load vector, error norms -------------
+   mfwq_quad_create   per-direction Gauss rule (gauss_pts_per_span points per knot span; <= 0 means p+1)
+                      and collocation tables          wq.py:41-49 gauss_points_weights, assembly.py:78-87
+   mfwq_quad_rhs      f_i = int det J b_i (f o F)       assembly.py:201-230 assemble_rhs
+   mfwq_quad_errors   err2, ref2 of the relative L2 / H1 error   problems.py:97-164 _error_integrals
+   Integrand: case_id MFWQ_CASE_CUBE_SINE / MFWQ_CASE_RING_OSC are evaluated in the kernel at the mapped
+   Gauss points (problems.py:77-94); MFWQ_CASE_VALUES reads caller values at every Gauss point (device
+   arrays, q1 fastest: fvals [Ng]; error: u values [Ng] and grad u [Ng][3]).  Geometry: kind as for the
+   stiffness operator; affine12 = A (row-major 3x3) then b (3) for MFWQ_GEOM_AFFINE; J_dev [Ng][9] for
+   MFWQ_GEOM_JACOBIAN (then the integrand must be MFWQ_CASE_VALUES).                                      */
+typedef struct mfwq_quad_s* mfwq_quad_t;
+#define MFWQ_CASE_VALUES 0
+#define MFWQ_CASE_CUBE_SINE 1
+#define MFWQ_CASE_RING_OSC 2
+int mfwq_quad_create(const int* p3, const int* nknots3, const double* const* knots3, int gauss_pts_per_span,
+                     mfwq_quad_t* out);
+/* ng3: Gauss points per direction; npts = prod ng3; ndofs = interior DoFs */
+int mfwq_quad_sizes(mfwq_quad_t q, int* ng3, long long* npts, long long* ndofs);
+/* host copy of the 1D Gauss points and weights of direction dir (ng3[dir] values each) */
+int mfwq_quad_points(mfwq_quad_t q, int dir, double* x, double* w);
+/* rhs_dev (ndofs) is overwritten */
+int mfwq_quad_rhs(mfwq_quad_t q, int kind, const double* affine12, const double* J_dev, int case_id,
+                  const double* fvals_dev, double* rhs_dev, void* stream);
+/* err_ref (host, 2 doubles) = {err2, ref2}; with_grad = 1: H1 (value + gradient terms), 0: L2.
+   Synchronises the stream. */
+int mfwq_quad_errors(mfwq_quad_t q, int kind, const double* affine12, const double* J_dev, int case_id,
+                     const double* uvals_dev, const double* gvals_dev, const double* u_dev, int with_grad,
+                     double* err_ref, void* stream);
+void mfwq_quad_destroy(mfwq_quad_t q);
+
 /* ---------------- fast diagonalisation preconditioner ---------------- */
 typedef struct mfwq_fd_s* mfwq_fd_t;
 /* K3/M3: host row-major (n_l x n_l) interior 1D stiffness / mass per direction */

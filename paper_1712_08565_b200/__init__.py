@@ -2,7 +2,8 @@
 
 Names mirror ``igamf/__init__.py:9-31`` for the path this package builds:
 setup (spaces, WQ rules, geometry maps), the matrix-free stiffness operator,
-the fast-diagonalisation preconditioner and PCG.  Compute runs in
+the fast-diagonalisation preconditioner, PCG / BiCGStab, and the tensor-Gauss
+load vector and L2 / H1 error norms.  Compute runs in
 hand-written sm_100a kernels (libmfwq.so, C-ABI in include/mfwq.h).
 """
 
@@ -10,6 +11,8 @@ from .errors import (DegenerateGeometryError, EigenSolveError,
                      IndefiniteOperatorError, WQConstructionError)
 from .geometry import GeometryMap, affine_map, identity_map, quarter_ring_map
 from .kron import CostMeter, kron_apply, tensor_grid
+from .problems import (ManufacturedCase, assemble_rhs, cube_sine_case, h1_relative_error, l2_relative_error,
+                       oscillating_case)
 from .operators import (COEFF_EVAL_FLOPS, MassOperator, StiffnessOperator, SystemOperator, apply_system,
                         setup_mass, setup_stiffness)
 from .solvers import (FDPreconditioner, KrylovReport, bicgstab, cg, stopping_tolerance,

@@ -76,6 +76,13 @@ _SIGS = {
                                C.c_double, C.c_double, dp, C.c_void_p]),
     "mfwq_kron_apply": (C.c_int, [C.c_int, ip, ip, C.POINTER(dp), C.c_void_p, C.c_void_p, C.c_int,
                                   C.c_void_p]),
+    "mfwq_quad_create": (C.c_int, [ip, ip, C.POINTER(dp), C.c_int, C.POINTER(C.c_void_p)]),
+    "mfwq_quad_sizes": (C.c_int, [C.c_void_p, ip, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "mfwq_quad_points": (C.c_int, [C.c_void_p, C.c_int, dp, dp]),
+    "mfwq_quad_rhs": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mfwq_quad_errors": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int, dp, C.c_void_p]),
+    "mfwq_quad_destroy": (None, [C.c_void_p]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -10,6 +10,7 @@ using namespace mfwq;
 struct mfwq_rule1d_s { Rule1D r; int nfun; };
 struct mfwq_stiffness_s { Stiffness op; };
 struct mfwq_fd_s { FastDiag fd; };
+struct mfwq_quad_s { Quadrature q; };
 
 static thread_local std::string g_err;
 long long mfwq::g_launches = 0;
@@ -283,4 +284,39 @@ int mfwq_bicg_xr(double* x, double* r, const double* phat, const double* shat, c
   return guard([&] { *rr = bicg_xr(x, r, phat, shat, s, t, n, alpha, omega, (cudaStream_t)stream); });
 }
 
+
+int mfwq_quad_create(const int* p3, const int* nknots3, const double* const* knots3, int gpts, mfwq_quad_t* out) {
+  return guard([&] { *out = new mfwq_quad_s{Quadrature(p3, nknots3, knots3, gpts)}; });
+}
+
+int mfwq_quad_sizes(mfwq_quad_t h, int* ng3, long long* npts, long long* ndofs) {
+  return guard([&] {
+    for (int l = 0; l < 3; ++l) ng3[l] = h->q.dir[l].n_el * h->q.g;
+    *npts = h->q.n_points();
+    *ndofs = h->q.n_dofs();
+  });
+}
+
+int mfwq_quad_points(mfwq_quad_t h, int dir, double* x, double* w) {
+  return guard([&] {
+    if (dir < 0 || dir > 2) throw ValueErr("direction must be 0, 1 or 2");
+    std::memcpy(x, h->q.dir[dir].x.data(), h->q.dir[dir].x.size() * sizeof(double));
+    std::memcpy(w, h->q.dir[dir].w.data(), h->q.dir[dir].w.size() * sizeof(double));
+  });
+}
+
+int mfwq_quad_rhs(mfwq_quad_t h, int kind, const double* affine12, const double* J_dev, int case_id,
+                  const double* fvals_dev, double* rhs_dev, void* stream) {
+  return guard([&] { h->q.rhs(kind, affine12, J_dev, case_id, fvals_dev, rhs_dev, (cudaStream_t)stream); });
+}
+
+int mfwq_quad_errors(mfwq_quad_t h, int kind, const double* affine12, const double* J_dev, int case_id,
+                     const double* uvals_dev, const double* gvals_dev, const double* u_dev, int with_grad,
+                     double* err_ref, void* stream) {
+  return guard([&] {
+    h->q.errors(kind, affine12, J_dev, case_id, uvals_dev, gvals_dev, u_dev, with_grad, err_ref, (cudaStream_t)stream);
+  });
+}
+
+void mfwq_quad_destroy(mfwq_quad_t h) { delete h; }
 }  // extern "C"

@@ -140,4 +140,28 @@ double bicg_xr(double* x, double* r, const double* ph, const double* sh, const d
                double alpha, double omega, cudaStream_t s);
 void axpy(double* y, const double* x, long long N, double a, cudaStream_t s);
 
+// Tensor-Gauss quadrature on the device (assembly.py:201-230, problems.py:97-164): load vector
+// and L2 / H1 error integrals, sum-factorised over element blocks (csrc/quadrature.cu).
+struct Quadrature {
+  struct QDir {
+    int n_el = 0, nfull = 0;
+    std::vector<double> x, w;
+    std::vector<int> first;  // first full basis index of each element
+    DevBuf<double> x_d, w_d, B_d;
+    DevBuf<int> first_d;
+  };
+  QDir dir[3];
+  int deg = 0, g = 0;
+  DevBuf<double> part_;
+  Quadrature(const int* p, const int* nknots, const double* const* knots, int gauss_per_span);
+  long long n_points() const;
+  long long n_dofs() const;
+  int window_max(int eb) const;
+  void pick_block(bool err, int& eb, int& w, size_t& smem) const;
+  void rhs(int kind, const double* affine12, const double* J_dev, int case_id, const double* fvals, double* out,
+           cudaStream_t s);
+  void errors(int kind, const double* affine12, const double* J_dev, int case_id, const double* uvals,
+              const double* gvals, const double* u, int with_grad, double* err_ref, cudaStream_t s);
+};
+
 }  // namespace mfwq

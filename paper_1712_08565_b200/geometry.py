@@ -20,6 +20,7 @@ class GeometryMap:
     _map: Callable
     _jacobian: Callable
     A: Optional[np.ndarray] = None
+    b: Optional[np.ndarray] = None
 
     def evaluate(self, xi):
         return self._map(np.atleast_2d(np.asarray(xi, dtype=float)))
@@ -42,7 +43,7 @@ def affine_map(A, b) -> GeometryMap:
     if np.linalg.det(A) <= 0:
         raise ValueError("affine map must be orientation-preserving")
     return GeometryMap(d, "affine", lambda xi: xi @ A.T + b,
-                       lambda xi: np.broadcast_to(A, (len(xi), d, d)).copy(), A=A)
+                       lambda xi: np.broadcast_to(A, (len(xi), d, d)).copy(), A=A, b=b)
 
 
 def quarter_ring_map() -> GeometryMap:
