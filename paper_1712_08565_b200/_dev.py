@@ -22,6 +22,10 @@ def is_device_tensor(v):
     return torch is not None and isinstance(v, torch.Tensor) and v.is_cuda
 
 
+def is_pinned_host(v):
+    return torch is not None and isinstance(v, torch.Tensor) and not v.is_cuda and v.is_pinned()
+
+
 def to_device(v, n=None):
     """Return (contiguous fp64 CUDA tensor, came_from_host)."""
     require_cuda()

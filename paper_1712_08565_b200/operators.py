@@ -194,6 +194,8 @@ class StiffnessOperator:
 
     # -- apply (operators.py:185-204) -----------------------------------------
     def apply(self, v, meter: CostMeter | None = None, out=None):
+        if _dev.is_pinned_host(v):
+            return self._apply_pinned(v, meter, out)
         x, host = _dev.to_device(v, self._in_len)
         y = out if out is not None else _dev.empty(self._out_len)
         _lib.check(_lib.lib().mfwq_stiffness_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
@@ -203,6 +205,65 @@ class StiffnessOperator:
         return _dev.back(y, host)
 
     __call__ = apply
+
+    def apply_pipelined(self, v, out=None, meter: CostMeter | None = None):
+        """Streaming form of ``apply`` for pinned host tensors: H2D on one side stream, the kernel on
+        the current stream, D2H on another side stream, two staging buffers.  A sequence of calls keeps
+        both copy directions and the SMs busy at once.  Returns ``(out, event)``; ``out`` is valid once
+        ``event`` has completed (``event.synchronize()`` or ``torch.cuda.synchronize()``)."""
+        if not _dev.is_pinned_host(v):
+            raise ValueError("apply_pipelined takes a pinned host torch tensor")
+        return self._apply_pinned(v, meter, out, d2h_side=True)
+
+    def _apply_pinned(self, v, meter, out, d2h_side=False):
+        """Pinned host torch tensor in, pinned host tensor out, asynchronous like torch's non_blocking
+        copies: with d2h_side=False the result is valid once the current stream is synchronised.  The
+        input copy runs on a side stream into one of two device staging buffers, so consecutive calls
+        overlap the H2D of call k+1 with the kernel and the D2H of call k."""
+        torch = _dev.torch
+        if v.numel() != self._in_len:
+            raise ValueError(f"expected vector of length {self._in_len}, got {v.numel()}")
+        st = getattr(self, "_pipe", None)
+        if st is None:
+            st = self._pipe = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
+                               "x": [_dev.empty(self._in_len) for _ in range(2)],
+                               "y": [_dev.empty(self._out_len) for _ in range(2)], "free": [None, None],
+                               "read": [None, None], "i": 0}
+        i = st["i"]
+        st["i"] ^= 1
+        cur = torch.cuda.current_stream()
+        h2d = st["h2d"]
+        if st["free"][i] is not None:
+            h2d.wait_event(st["free"][i])  # the kernel that last read this staging buffer is done
+        with torch.cuda.stream(h2d):
+            st["x"][i].copy_(v.reshape(-1).to(torch.float64), non_blocking=True)
+            landed = torch.cuda.Event()
+            landed.record(h2d)
+        cur.wait_event(landed)
+        if st["read"][i] is not None:
+            cur.wait_event(st["read"][i])  # the side-stream D2H that last read this staging buffer is done
+        _lib.check(_lib.lib().mfwq_stiffness_apply(self._h, C.c_void_p(st["x"][i].data_ptr()),
+                                                   C.c_void_p(st["y"][i].data_ptr()), C.c_void_p(cur.cuda_stream)))
+        free = torch.cuda.Event()
+        free.record(cur)
+        st["free"][i] = free
+        o = out if out is not None else torch.empty(self._out_len, dtype=torch.float64, pin_memory=True)
+        if o.numel() != self._out_len or o.is_cuda:
+            raise ValueError("out must be a host tensor of the output length")
+        if meter is not None:
+            meter.add_flops(self.apply_flops)
+        if not d2h_side:
+            o.reshape(-1).copy_(st["y"][i], non_blocking=True)
+            st["read"][i] = None
+            return o
+        d2h = st["d2h"]
+        d2h.wait_event(free)
+        with torch.cuda.stream(d2h):
+            o.reshape(-1).copy_(st["y"][i], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(d2h)
+        st["read"][i] = done
+        return o, done
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -156,3 +156,35 @@ def test_torch_device_inputs_stay_on_device():
     y = A.apply(x)
     assert isinstance(y, torch.Tensor) and y.is_cuda
     assert relerr(y.cpu().numpy(), A.apply(x.cpu().numpy())) <= 1e-14  # fp64 atomics: order-dependent rounding
+
+
+def test_pinned_host_apply_is_pipelined_and_exact():
+    """Pinned host tensors take the asynchronous path (side-stream H2D, double-buffered staging):
+    after a stream sync every result equals the device-path result."""
+    import torch
+    space = M.tensor_space(3, 6)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map())
+    xs = [torch.from_numpy(np.random.default_rng(s).standard_normal(space.n_dofs)).pin_memory() for s in range(5)]
+    outs = [torch.empty(space.n_dofs, dtype=torch.float64, pin_memory=True) for _ in xs]
+    for x, o in zip(xs, outs):
+        assert A.apply(x, out=o) is o
+    torch.cuda.current_stream().synchronize()
+    for x, o in zip(xs, outs):
+        ref = A.apply(x.numpy())
+        assert relerr(o.numpy(), ref) <= 1e-14
+    auto = A.apply(xs[0])  # allocates a pinned result
+    torch.cuda.current_stream().synchronize()
+    assert auto.is_pinned() and relerr(auto.numpy(), A.apply(xs[0].numpy())) <= 1e-14
+
+
+def test_apply_pipelined_matches():
+    import torch
+    space = M.tensor_space(2, 7)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.identity_map(3))
+    xs = [torch.from_numpy(np.random.default_rng(s).standard_normal(space.n_dofs)).pin_memory() for s in range(4)]
+    res = [A.apply_pipelined(x) for x in xs]
+    for (o, ev), x in zip(res, xs):
+        ev.synchronize()
+        assert relerr(o.numpy(), A.apply(x.numpy())) <= 1e-14
+    with pytest.raises(ValueError):
+        A.apply_pipelined(np.zeros(space.n_dofs))
