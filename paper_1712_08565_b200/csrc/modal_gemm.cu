@@ -17,7 +17,7 @@
 namespace mfwq {
 namespace mg {
 
-constexpr int BK = 16, APAD = 4, BPAD = 8, STAGES = 3;
+constexpr int BK = 16, APAD = 4, BPAD = 4, STAGES = 3;  // BN + 4 = 4 mod 16: conflict-free [k][n] B fragments
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
