@@ -101,7 +101,7 @@ struct Params {
 
 
 struct Maps {
-  CUtensorMap m[6];  // per coefficient grid, 16 x 16 x 1 boxes (zero fill past the grid edge)
+  CUtensorMap m[12];  // per coefficient grid: 16 x 16 x 4 boxes, then 16 x 16 x 2 boxes (zero fill past the grid edge)
 };
 
 template <int NT>
@@ -194,11 +194,20 @@ __device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map,
 // ---- the kernel ----------------------------------------------------------------
 // CTAs per SM: 2 where the register state (ring 3(p+1) + accumulators NT(p+3) doubles) fits
 // 128 registers without spilling, else 1 with up to 255 registers
+// z-elements per step: 2, except the 5-term kernel at p = 3, where one element per step halves the
+// stage buffers so that two CTAs fit in shared memory (ring p = 3: 2.78 -> 2.53 ms at n_el = 256;
+// at p = 4 the same change spills and measured no faster, 2.89 vs 2.94 ms)
+__host__ __device__ constexpr int zs_for(int p, int nt) {
+#ifdef MFWQ_NT5_ZS2  // timing experiments only
+  return 2;
+#endif
+  return (nt == 5 && p == 3) ? 1 : 2;
+}
 __host__ __device__ constexpr int occ_for(int p, int nt) {
 #ifdef MFWQ_OCC6
   if (nt == 3 && p == MFWQ_OCCP) return MFWQ_OCC6;
 #endif
-  return ((nt == 3 && p <= 6) || (nt == 5 && p <= 2)) ? 2 : 1;
+  return ((nt == 3 && p <= 6) || (nt == 5 && (p <= 2 || zs_for(p, nt) == 1))) ? 2 : 1;
 }
 template <int P, int NT>
 struct Occ {
@@ -256,7 +265,7 @@ struct Smem {
   static constexpr int FPT = (DMAX * DMAX + NTHR - 1) / NTHR;       // v-window cells per thread
   static size_t bytes(int qe, int max_chunk) {
     return sizeof(double) * (size_t)(oZ + ZS * qe * ZT) + sizeof(int) * 2 * TQ + 16 + 32 + sizeof(int) * (max_chunk + 2) +
-           sizeof(int) * FPT * NTHR + sizeof(int) * (max_chunk / 2 + 2);
+           sizeof(int) * FPT * NTHR + sizeof(int) * (max_chunk / ZS + 2);
   }
 };
 
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   // arm_stage (thread 0, once the previous phase has completed) sets the transaction bytes;
   // issue_stage (after the barrier that frees sC / sZ) spreads the copies over warps 0..G, lane 0
   // each: warp 0 the bulk z rows, warp 1 + slot one 16 x 16 x 4 coefficient box per used grid
-  static_assert(ZS == 2, "one 16 x 16 x 4 box per grid covers a regular step's 2 x 2 planes");
+  static_assert(ZS == 1 || ZS == 2, "one 16 x 16 x 2ZS box per grid covers a regular step's ZS x 2 planes");
   auto arm_stage = [&](int el, int nz) {
     if (tid != 0) return;
     const bool tma = !OTF && nz == ZS && sStep[el / ZS];
@@ -398,13 +407,13 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     const int qa = sQ0[el];
     if (warp == 0) {
       bulk_load(sZ, prm.ztab + (size_t)qa * ZT, (unsigned)((sQ0[el + nz] - qa) * ZT * 8), &mbar[0]);
-    } else if (!OTF && nz == ZS && sStep[el / ZS]) {  // regular step: planes qa .. qa+3 -> sC [slot][plane][256]
+    } else if (!OTF && nz == ZS && sStep[el / ZS]) {  // regular step: planes qa .. qa+2ZS-1 -> sC [slot][plane][256]
       const int sl = warp - 1;
       int g = 0;
 #pragma unroll
       for (int h = 0; h < 6; ++h)
         if (grid_used<NT>(h) && grid_slot<NT>(h) == sl) g = h;
-      tma_load_3d(sC + sl * (2 * ZS) * 256, &maps.m[g], sInf->q0x, sInf->q0y, qa - prm.qzb, &mbar[0]);
+      tma_load_3d(sC + sl * (2 * ZS) * 256, &maps.m[(ZS == 2 ? 0 : 6) + g], sInf->q0x, sInf->q0y, qa - prm.qzb, &mbar[0]);
     }
   };
   // a step takes its coefficients by TMA when it has ZS elements of exactly 2 planes each
@@ -792,7 +801,7 @@ struct Fused2Plan {
   int ntile[3] = {0, 0, 0};
   int max_nqz = 0, qe = 0, max_chunk = 0;
   const double* maps_for = nullptr;  // coefficient buffer the maps were encoded for
-  f2::Maps maps;  // 16 x 16 x 4 boxes: the 2 x 2 planes of a regular step
+  f2::Maps maps;  // 16 x 16 x 4 / x 2 boxes: the ZS x 2 planes of a regular step
 };
 
 bool build_elem_tables(const Dir1D& d, std::vector<double>& B, std::vector<double>& W, std::vector<int>& eq);
@@ -949,12 +958,13 @@ void encode_maps(Stiffness& S, Fused2Plan& F) {
   if (F.maps_for == S.coeff.ptr) return;
   auto enc = get_encode();
   const size_t G = S.grid_elems();
-  for (int g = 0; g < 6; ++g) {
+  for (int mi = 0; mi < 12; ++mi) {
+    const int g = mi % 6;
     cuuint64_t dims[3] = {(cuuint64_t)S.dir[0].m, (cuuint64_t)S.dir[1].m, (cuuint64_t)(S.q_hi - S.q_lo)};
     cuuint64_t strides[2] = {(cuuint64_t)S.m1p * 8, (cuuint64_t)S.m1p * S.dir[1].m * 8};
-    cuuint32_t box[3] = {(cuuint32_t)f2::TQ, (cuuint32_t)f2::TQ, 4};  // the 2 x 2 planes of a regular step
+    cuuint32_t box[3] = {(cuuint32_t)f2::TQ, (cuuint32_t)f2::TQ, mi < 6 ? 4u : 2u};  // the ZS x 2 planes of a step
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&F.maps.m[g], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(S.coeff.ptr + g * G), dims,
+    CUresult r = enc(&F.maps.m[mi], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(S.coeff.ptr + g * G), dims,
                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaErr("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
@@ -968,7 +978,7 @@ void encode_maps(Stiffness& S, Fused2Plan& F);
 
 template <int P, int NT, bool OTF>
 static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
-  constexpr int ZS = 2;
+  constexpr int ZS = f2::zs_for(P, NT);
   using namespace f2;
   if constexpr (!OTF) encode_maps(S, F);
   Params prm;
