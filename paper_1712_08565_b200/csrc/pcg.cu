@@ -3,6 +3,7 @@
 // reads back two scalars (p.Ap and ||r||^2) for the indefiniteness and
 // stopping tests, exactly where the reference takes those decisions.
 #include <cmath>
+#include <cstdint>
 
 #include "ops.h"
 
@@ -41,16 +42,47 @@ __global__ void __launch_bounds__(RB) finish_sum(const double* __restrict__ part
 }
 
 // x += alpha p ; r -= alpha Ap ; partial ||r||^2     (alpha = sc[0] / sc[1])
+// 16-byte accesses, two pairs per thread per trip (all vectors 16-byte aligned; the odd tail
+// element, if any, is done by the last thread of block 0).  Summation order of the partials is
+// fixed by the grid, so the result is deterministic.
 __global__ void __launch_bounds__(RB) update_xr(double* __restrict__ x, double* __restrict__ r,
                                                 const double* __restrict__ p, const double* __restrict__ Ap,
                                                 long long N, const double* __restrict__ rz,
                                                 const double* __restrict__ pAp, double* __restrict__ partial) {
   const double alpha = *rz / *pAp;
   double s = 0.0;
-  for (long long i = blockIdx.x * (long long)RB + threadIdx.x; i < N; i += (long long)gridDim.x * RB) {
-    x[i] += alpha * p[i];
-    const double ri = r[i] - alpha * Ap[i];
-    r[i] = ri;
+  const long long N2 = N >> 1, stride = (long long)gridDim.x * RB;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* a2 = reinterpret_cast<const double2*>(Ap);
+  long long i = blockIdx.x * (long long)RB + threadIdx.x;
+  for (; i + stride < N2; i += 2 * stride) {
+    const double2 xa = x2[i], xb = x2[i + stride], pa = p2[i], pb = p2[i + stride];
+    const double2 ra = r2[i], rb = r2[i + stride], aa = a2[i], ab = a2[i + stride];
+    x2[i] = make_double2(xa.x + alpha * pa.x, xa.y + alpha * pa.y);
+    x2[i + stride] = make_double2(xb.x + alpha * pb.x, xb.y + alpha * pb.y);
+    const double2 na = make_double2(ra.x - alpha * aa.x, ra.y - alpha * aa.y);
+    const double2 nb = make_double2(rb.x - alpha * ab.x, rb.y - alpha * ab.y);
+    r2[i] = na;
+    r2[i + stride] = nb;
+    s += na.x * na.x;
+    s += na.y * na.y;
+    s += nb.x * nb.x;
+    s += nb.y * nb.y;
+  }
+  for (; i < N2; i += stride) {
+    const double2 xa = x2[i], pa = p2[i], ra = r2[i], aa = a2[i];
+    x2[i] = make_double2(xa.x + alpha * pa.x, xa.y + alpha * pa.y);
+    const double2 na = make_double2(ra.x - alpha * aa.x, ra.y - alpha * aa.y);
+    r2[i] = na;
+    s += na.x * na.x;
+    s += na.y * na.y;
+  }
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == RB - 1) {
+    x[N - 1] += alpha * p[N - 1];
+    const double ri = r[N - 1] - alpha * Ap[N - 1];
+    r[N - 1] = ri;
     s += ri * ri;
   }
   s = block_sum(s);
@@ -61,8 +93,20 @@ __global__ void __launch_bounds__(RB) update_xr(double* __restrict__ x, double* 
 __global__ void __launch_bounds__(RB) update_p(double* __restrict__ p, const double* __restrict__ z, long long N,
                                                const double* __restrict__ rz_new, const double* __restrict__ rz) {
   const double beta = *rz_new / *rz;
-  for (long long i = blockIdx.x * (long long)RB + threadIdx.x; i < N; i += (long long)gridDim.x * RB)
-    p[i] = z[i] + beta * p[i];
+  const long long N2 = N >> 1, stride = (long long)gridDim.x * RB;
+  double2* p2 = reinterpret_cast<double2*>(p);
+  const double2* z2 = reinterpret_cast<const double2*>(z);
+  long long i = blockIdx.x * (long long)RB + threadIdx.x;
+  for (; i + stride < N2; i += 2 * stride) {
+    const double2 pa = p2[i], pb = p2[i + stride], za = z2[i], zb = z2[i + stride];
+    p2[i] = make_double2(za.x + beta * pa.x, za.y + beta * pa.y);
+    p2[i + stride] = make_double2(zb.x + beta * pb.x, zb.y + beta * pb.y);
+  }
+  for (; i < N2; i += stride) {
+    const double2 pa = p2[i], za = z2[i];
+    p2[i] = make_double2(za.x + beta * pa.x, za.y + beta * pa.y);
+  }
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == RB - 1) p[N - 1] = z[N - 1] + beta * p[N - 1];
 }
 
 __global__ void copy_scalar(const double* src, double* dst) { *dst = *src; }
@@ -87,12 +131,29 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
   out = KrylovOut{};
   MFWQ_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s));
   // persistent workspace on the operator (no cudaMalloc/cudaFree inside the solve)
-  A.pcg_ws.alloc_at_least(4 * N + RGRID + 4);
+  // work vectors at a 32-double pitch: every one 256-byte aligned for the 16-byte update kernels
+  const long long NP = (N + 31) & ~31LL;
+  const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  A.pcg_ws.alloc_at_least(x_aligned ? 4 * NP + RGRID + 4 : 5 * NP + 640);
   double* r = A.pcg_ws.ptr;
-  double* z = r + N;
-  double* p = z + N;
-  double* Ap = p + N;
-  struct { double* ptr; } part{Ap + N}, sc{Ap + N + RGRID};  // sc: 0 rz, 1 pAp, 2 rr, 3 rz_new
+  double* z = r + NP;
+  double* p = z + NP;
+  double* Ap = p + NP;
+  double* const x_out = x;
+  if (!x_aligned) {  // iterate in an aligned copy, hand the result back at the end
+    x = r + 4 * NP + 640;  // 32-double aligned slot after the partials and scalars
+    MFWQ_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s));
+  }
+  struct CopyBack {
+    double* dst;
+    const double* src;
+    long long n;
+    cudaStream_t s;
+    ~CopyBack() {
+      if (dst != src) cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    }
+  } copy_back{x_out, x, N, s};
+  struct { double* ptr; } part{Ap + NP}, sc{Ap + NP + RGRID};  // sc: 0 rz, 1 pAp, 2 rr, 3 rz_new
   double* rz = sc.ptr;
   double* pAp = sc.ptr + 1;
   double* rr = sc.ptr + 2;
@@ -114,6 +175,29 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
   MFWQ_CUDA(cudaMemcpyAsync(p, z, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
   dot_to(r, z, N, part.ptr, rz, s);
   hist.push_back(1.0);
+  // The next preconditioner apply (and its r.z / p update) is enqueued BEFORE the host reads the
+  // iteration's scalars whenever the last residual is far above tol: the device then never idles
+  // through the host round trip.  The arithmetic and its order are unchanged; on a (rare) wrong
+  // guess the extra work is simply dropped (counters count only what the reference would do).
+  bool ahead = false;  // P(r), r.z, p-update of this iteration already enqueued
+  double last_rel = 1.0;
+  auto enqueue_precond = [&]() {
+    if (P) P->apply(r, z, s);
+    else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    dot_to(r, z, N, part.ptr, rzn, s);
+    update_p<<<RGRID, RB, 0, s>>>(p, z, N, rzn, rz); note_launch();
+    copy_scalar<<<1, 1, 0, s>>>(rzn, rz); note_launch();
+    MFWQ_CUDA(cudaGetLastError());
+  };
+  cudaEvent_t ev;
+  MFWQ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  double* hsc = nullptr;
+  MFWQ_CUDA(cudaMallocHost(&hsc, 2 * sizeof(double)));
+  struct Cleanup {
+    cudaEvent_t e;
+    double* h;
+    ~Cleanup() { cudaEventDestroy(e); cudaFreeHost(h); }
+  } cleanup{ev, hsc};
   for (int k = 1; k <= maxit; ++k) {
     A.apply(p, Ap, s);
     out.matvecs++;
@@ -121,28 +205,33 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
     update_xr<<<RGRID, RB, 0, s>>>(x, r, p, Ap, N, rz, pAp, part.ptr); note_launch();
     finish_sum<<<1, RB, 0, s>>>(part.ptr, RGRID, rr); note_launch();
     MFWQ_CUDA(cudaGetLastError());
-    MFWQ_CUDA(cudaMemcpyAsync(h2, pAp, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    MFWQ_CUDA(cudaStreamSynchronize(s));
+    MFWQ_CUDA(cudaMemcpyAsync(hsc, pAp, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MFWQ_CUDA(cudaEventRecord(ev, s));
+    // PCG reduces the residual by a bounded factor per step: far from tol, the next step is certain
+    ahead = k < maxit && last_rel > 1e3 * tol;
+    if (ahead) enqueue_precond();
+    MFWQ_CUDA(cudaEventSynchronize(ev));
+    h2[0] = hsc[0];
+    h2[1] = hsc[1];
     if (h2[0] <= 0) {  // solvers.py:156-160
       char m[128];
       snprintf(m, sizeof m, "nonpositive curvature p.Ap = %.3e at iteration %d", h2[0], k);
+      MFWQ_CUDA(cudaStreamSynchronize(s));
       throw IndefiniteErr(m);
     }
     const double rel = std::sqrt(h2[1]) / bnorm;
     hist.push_back(rel);
+    last_rel = rel;
     if (rel <= tol) {
+      MFWQ_CUDA(cudaStreamSynchronize(s));  // a speculative step may still be running on x's stream
       out.iterations = k;
       out.converged = 1;
       return;
     }
-    if (P) P->apply(r, z, s);
-    else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (!ahead) enqueue_precond();
     out.precs++;
-    dot_to(r, z, N, part.ptr, rzn, s);
-    update_p<<<RGRID, RB, 0, s>>>(p, z, N, rzn, rz); note_launch();
-    copy_scalar<<<1, 1, 0, s>>>(rzn, rz); note_launch();
-    MFWQ_CUDA(cudaGetLastError());
   }
+  MFWQ_CUDA(cudaStreamSynchronize(s));
   out.iterations = maxit;
   out.converged = 0;
 }

@@ -188,3 +188,33 @@ def test_apply_pipelined_matches():
         assert relerr(o.numpy(), A.apply(x.numpy())) <= 1e-14
     with pytest.raises(ValueError):
         A.apply_pipelined(np.zeros(space.n_dofs))
+
+
+def test_pcg_c_abi_unaligned_solution_buffer():
+    """mfwq_pcg_solve with x 8 bytes off a 16-byte boundary and odd N (the vectorised update
+    kernels iterate in an aligned copy and hand the result back) equals the aligned call."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1712_08565_b200 import _dev, _lib
+
+    space = M.tensor_space(3, 6)  # n = 7 per direction: N = 343, odd
+    assert space.n_dofs % 2 == 1
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map())
+    P = M.FDPreconditioner(space)
+    b = np.random.default_rng(1).standard_normal(space.n_dofs)
+    u_ref, rep_ref = M.cg(A.apply, b, P.apply, tol=1e-10)
+    bt = torch.from_numpy(b).cuda()
+    buf = torch.zeros(space.n_dofs + 1, dtype=torch.float64, device="cuda")
+    x = buf[1:]
+    assert x.data_ptr() % 16 == 8
+    hist = np.zeros(1002)
+    rep = _lib.KrylovReportC()
+    _lib.check(_lib.lib().mfwq_pcg_solve(A._h, P._h, C.c_void_p(bt.data_ptr()), C.c_void_p(x.data_ptr()),
+                                         1e-10, 1000, _lib.dptr(hist), C.byref(rep),
+                                         C.c_void_p(_dev.stream_ptr())))
+    torch.cuda.synchronize()
+    assert rep.iterations == rep_ref.iterations and bool(rep.converged)
+    assert relerr(x.cpu().numpy(), u_ref) <= 1e-13
+    assert float(buf[0]) == 0.0
