@@ -335,13 +335,16 @@ def run_ours(args, rank, world, local):
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, min(args.steps, 20))  # long enough to amortise the pipeline fill and drain
     e0.record(stream)
+    last = {}
     for _ in range(e2e_steps):
         for p in SWEEP:
             # pinned host x -> H2D (side stream) -> kernel -> D2H (side stream) into pinned host y:
             # consecutive calls overlap the two copy directions and the kernels
-            ops[p]["A"].apply_pipelined(hx[p], out=hy[p])
+            _, last[p] = ops[p]["A"].apply_pipelined(hx[p], out=hy[p])
+    for p in SWEEP:  # the timed region ends when the last result has landed in host memory
+        stream.wait_event(last[p])
     e1.record(stream)
     torch.cuda.synchronize()
     for p in SWEEP:  # the host results are the device results
@@ -353,6 +356,7 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = dofs_step * e2e_steps * world / (float(e2e_t) * 1e-3)
+    pcie = pcie_probe(torch, hx, ops, stream)
 
     # on-the-fly coefficients (reference on_the_fly=True, operators.py:171-183): same sweep with C
     # evaluated in-kernel from C(xi1) instead of read from the N_q grids (secondary figure)
@@ -419,7 +423,7 @@ def run_ours(args, rank, world, local):
                 "per_degree_dofs": {str(p): ops[p]["N"] for p in SWEEP},
                 "roofline": roof,
                 "cpu_baseline": cpu,
-                "e2e": {"value": e2e_value, "unit": UNIT,
+                "e2e": {"value": e2e_value, "unit": UNIT, "pcie": pcie,
                         "h2d_bytes_per_step": 8 * dofs_step, "d2h_bytes_per_step": 8 * dofs_step},
                 "gpu_launches": int(launches),
                 "clocks": clk.summary(),
@@ -509,6 +513,34 @@ def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1, otf=False):
             "setup_s": {"wq_rule": t1 - t0, "coeff_grids": t2 - t1, "fd": t3 - t2},
             "fd_apply": fd,
             "u_norm": float(torch.linalg.vector_norm(u))}
+
+
+def pcie_probe(torch, hx, ops, stream):
+    """Host<->device copy bandwidth with the e2e step's own pinned buffers: one direction alone and
+    both at once (the ceiling of the pipelined e2e figure, which moves 2 x 88 MB per step)."""
+    dx = {p: ops[p]["x"] for p in SWEEP}
+    hy = {p: torch.empty_like(hx[p]).pin_memory() for p in SWEEP}
+    nbytes = sum(hx[p].numel() * 8 for p in SWEEP)
+    s2 = torch.cuda.Stream()
+    res = {}
+    for mode in ("h2d", "d2h", "both"):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        s2.wait_stream(stream)
+        for p in SWEEP:
+            if mode in ("h2d", "both"):
+                with torch.cuda.stream(stream):
+                    dx[p].copy_(hx[p], non_blocking=True)
+            if mode in ("d2h", "both"):
+                with torch.cuda.stream(s2):
+                    hy[p].copy_(ops[p]["y"], non_blocking=True)
+        stream.wait_stream(s2)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        res[mode + "_gbs"] = (2 if mode == "both" else 1) * nbytes / (ms * 1e-3) / 1e9
+    return res
 
 
 def run_pcg(M, torch, dev, otf=False):
