@@ -10,6 +10,8 @@
 #include "rule1d.h"
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <stdexcept>
 #include <string>
@@ -226,15 +228,15 @@ static Csr wq_matrix(const Knots& kv, const std::vector<double>& pts, int a, int
   for (int q = 0; q < nq; ++q)
     for (int u = Cb.indptr[q]; u < Cb.indptr[q + 1]; ++u) colb[size_t(Cb.indices[u]) * nq + q] = Cb.data[u];
   std::vector<double> G = exact_gram(kv, a, b);
-  Csr W;
-  W.rows = n;
-  W.cols = nq;
-  W.indptr.assign(1, 0);
-  std::vector<int> qs, js;
-  std::vector<double> E, g, w;
-  for (int i = 0; i < n; ++i) {
+  // rows are independent least-squares problems: solve them on all host cores, then assemble the
+  // CSR in row order and report the first failing row, exactly like the sequential loop
+  std::vector<std::vector<int>> rq(n);
+  std::vector<std::vector<double>> rw(n);
+  std::vector<double> rres(n, 0.0);
+  auto solve_row = [&](int i, std::vector<double>& E, std::vector<double>& g, std::vector<int>& js) {
     double lo = kv.t[i], hi = kv.t[i + kv.p + 1];
-    qs.clear(); js.clear();
+    std::vector<int>& qs = rq[i];
+    js.clear();
     for (int q = 0; q < nq; ++q)
       if (pts[q] >= lo - 1e-14 && pts[q] <= hi + 1e-14) qs.push_back(q);
     for (int j = 0; j < n; ++j)
@@ -242,6 +244,7 @@ static Csr wq_matrix(const Knots& kv, const std::vector<double>& pts, int a, int
     const int r = int(js.size()), c = int(qs.size());
     E.assign(size_t(r) * c, 0.0);
     g.assign(r, 0.0);
+    std::vector<double>& w = rw[i];
     w.assign(c, 0.0);
     for (int u = 0; u < r; ++u) {
       for (int v = 0; v < c; ++v) E[size_t(u) * c + v] = colb[size_t(js[u]) * nq + qs[v]];
@@ -254,8 +257,27 @@ static Csr wq_matrix(const Knots& kv, const std::vector<double>& pts, int a, int
       for (int v = 0; v < c; ++v) acc += E[size_t(u) * c + v] * w[v];
       res = std::max(res, std::fabs(acc - g[u]));
     }
-    if (res > kExactnessTol) throw WQFail{i, res};
-    for (int v = 0; v < c; ++v) { W.indices.push_back(qs[v]); W.data.push_back(w[v]); }
+    rres[i] = res;
+  };
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nth = int(std::min<unsigned>(hw, unsigned(std::max(1, n / 16))));
+  std::atomic<int> next{0};
+  auto worker = [&]() {
+    std::vector<double> E, g;
+    std::vector<int> js;
+    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) solve_row(i, E, g, js);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nth; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  Csr W;
+  W.rows = n;
+  W.cols = nq;
+  W.indptr.assign(1, 0);
+  for (int i = 0; i < n; ++i) {
+    if (rres[i] > kExactnessTol) throw WQFail{i, rres[i]};
+    for (size_t v = 0; v < rq[i].size(); ++v) { W.indices.push_back(rq[i][v]); W.data.push_back(rw[i][v]); }
     W.indptr.push_back(int(W.indices.size()));
   }
   return W;
