@@ -201,11 +201,20 @@ __host__ __device__ constexpr int zs_for(int p, int nt) {
 #ifdef MFWQ_NT5_ZS2  // timing experiments only
   return 2;
 #endif
+#ifdef MFWQ_NT5_ZS1P4  // timing experiments only
+  if (nt == 5 && p == 4) return 1;
+#endif
+#ifdef MFWQ_NT3_ZS1  // timing experiments only: 3-term kernel, one element per step, 3 CTAs/SM
+  if (nt == 3 && p <= MFWQ_NT3_ZS1) return 1;
+#endif
   return (nt == 5 && p == 3) ? 1 : 2;
 }
 __host__ __device__ constexpr int occ_for(int p, int nt) {
 #ifdef MFWQ_OCC6
   if (nt == 3 && p == MFWQ_OCCP) return MFWQ_OCC6;
+#endif
+#ifdef MFWQ_NT3_ZS1
+  if (nt == 3 && p <= MFWQ_NT3_ZS1) return 3;
 #endif
   return ((nt == 3 && p <= 6) || (nt == 5 && (p <= 2 || zs_for(p, nt) == 1))) ? 2 : 1;
 }

@@ -95,3 +95,22 @@ def test_space_and_index_maps():
     assert sp.n_per_dir == (5, 5, 5) and sp.n_dofs == 125
     assert M.multi_to_scalar((2, 1, 1), (5, 5, 5)) == 2
     assert M.scalar_to_multi(M.multi_to_scalar((3, 4, 5), (5, 5, 5)), (5, 5, 5)) == (3, 4, 5)
+
+
+def test_bench_reference_arm_runs_on_host_cores():
+    """bench.py --impl reference: the CPU arm (oracle matvec processes on the host cores) prints one
+    JSON line in the driver's format, with its own e2e and cpu_baseline."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MFWQ_REF_WORKERS="2")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "1"], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "DoF/s" and line["value"] > 0
+    assert line["cpu_baseline"]["cores"] == 2 and line["cpu_baseline"]["kind"] == "port"
+    assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert set(line["per_degree_s"]) == {"2", "3"}
