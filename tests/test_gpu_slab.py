@@ -53,3 +53,33 @@ def test_fd_dir_ops_compose_to_apply():
     s = op(1, 1, 0, s, n3, n2, 0)
     s = op(0, 1, 0, s, n3, n2, 0)
     assert relerr(s.cpu().numpy(), P.apply(x).cpu().numpy()) <= 1e-13
+
+
+def test_distributed_pcg_single_rank_nccl():
+    """setup_distributed + dist_cg over a one-rank NCCL group on cuda:0 (the multi-GPU code path with
+    its collectives degenerate) equals the single-GPU device PCG: iterations and solution."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1712_08565_b200.dist import dist_cg, setup_distributed
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        p, n_el = 3, 12
+        space = M.tensor_space(p, n_el)
+        rule = M.build_tensor_rule(space)
+        A, P, part = setup_distributed(space, rule, M.quarter_ring_map())
+        assert part.owned(0) == (0, space.n_per_dir[2])
+        b = torch.from_numpy(np.random.default_rng(1).standard_normal(space.n_dofs)).cuda()
+        u, rep = dist_cg(A.apply, b, P.apply, tol=1e-8)
+        A1 = M.setup_stiffness(space, rule, M.quarter_ring_map())
+        u1, rep1 = M.cg(A1.apply, b, M.FDPreconditioner(space).apply, tol=1e-8)
+        assert rep.converged and abs(rep.iterations - rep1.iterations) <= 1
+        assert relerr(u.cpu().numpy(), u1.cpu().numpy()) <= 1e-9
+    finally:
+        dist.destroy_process_group()
