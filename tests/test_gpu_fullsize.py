@@ -47,3 +47,33 @@ def test_cfg4_pcg_anchor(p):
     assert rep.converged and abs(rep.iterations - iters) <= 1
     # anchors carry 11 digits; the solution itself is reproduced to the PCG tolerance
     assert abs(float(torch.linalg.vector_norm(u)) - unorm) <= 1e-9 * unorm
+
+
+# cfg 3 (quarter ring, p = 4, n_el = 256, 17.2 M DoFs): reference anchors of SURVEY §8(c) --
+# ||A x|| on x = default_rng(0), and the FD-PCG run on b = default_rng(1): 27 iterations, ||u||
+CFG3_AX, CFG3_U, CFG3_IT = 1.1566850369e+01, 9.9147347659e+07, 27
+
+
+@pytest.mark.parametrize("otf", [False, True])
+def test_cfg3_matvec_and_pcg_anchor(otf):
+    space = M.tensor_space(4, 256)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map(), on_the_fly=otf)
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(space.n_dofs)).cuda()
+    ax = float(torch.linalg.vector_norm(A.apply(x)))
+    assert abs(ax - CFG3_AX) <= 1e-10 * CFG3_AX  # anchor carries 11 digits
+    P = M.FDPreconditioner(space)
+    b = torch.from_numpy(np.random.default_rng(1).standard_normal(space.n_dofs)).cuda()
+    u, rep = M.cg(A.apply, b, P.apply, tol=1e-8)
+    assert rep.converged and abs(rep.iterations - CFG3_IT) <= 1
+    assert abs(float(torch.linalg.vector_norm(u)) - CFG3_U) <= 1e-9 * CFG3_U
+    assert rep.matvecs == rep.iterations == rep.precond_applies
+
+
+def test_fd_round_trip_cfg3_size():
+    """Size-independent property at the full cfg-3 size (n = 258): P^-1 (P v) = v (the reference's
+    self-inverse test, test_solvers.py:35-45, at 17.2 M DoFs)."""
+    space = M.tensor_space(4, 256)
+    P = M.FDPreconditioner(space)
+    v = torch.from_numpy(np.random.default_rng(0).standard_normal(space.n_dofs)).cuda()
+    back = P.apply(P.apply_forward(v))
+    assert float(torch.linalg.vector_norm(back - v)) <= 1e-10 * float(torch.linalg.vector_norm(v))
