@@ -81,13 +81,15 @@ __global__ void __launch_bounds__(WM * WN * 32, 2)
     bok[i] = n0 + bcc[i] < N;
     bcol[i] = bok[i] ? colpart(xv, n0 + bcc[i]) : 0;
   }
-  auto load = [&](int stage, int k0) {
+  auto load_a = [&](int stage, int k0) {
     double* as = As + stage * BM * PA;
     for (int e = tid; e < BM * (BK / 2); e += THREADS) {  // 16-byte copies: lda even, A zero-padded
       const int r = e / (BK / 2), c = 2 * (e % (BK / 2)), gm = m0 + r, gk = k0 + c;
       const bool ok = gm < M && gk < lda;
       cp16(as + r * PA + c, ok ? A + (long long)gm * lda + gk : A, ok);
     }
+  };
+  auto load_b = [&](int stage, int k0) {
     double* bs = Bs + stage * BSZ;
 #pragma unroll
     for (int i = 0; i < BPER; ++i) {
@@ -113,9 +115,15 @@ __global__ void __launch_bounds__(WM * WN * 32, 2)
     for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (K + BK - 1) / BK;
+  // The factor A never depends on the previous kernel: its first stages are fetched before waiting
+  // on the preceding grid (programmatic dependent launch), X only after it has completed.
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s)
+    if (s < nk) load_a(s, s * BK);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load(s, s * BK);
+    if (s < nk) load_b(s, s * BK);
     commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -123,7 +131,10 @@ __global__ void __launch_bounds__(WM * WN * 32, 2)
     __syncthreads();
     {  // prefetch k-tile kt + STAGES - 1 into the slot freed at kt - 1
       const int kn = kt + STAGES - 1;
-      if (kn < nk) load(kn % STAGES, kn * BK);
+      if (kn < nk) {
+        load_a(kn % STAGES, kn * BK);
+        load_b(kn % STAGES, kn * BK);
+      }
       commit();
     }
     const double* as = As + (kt % STAGES) * BM * PA + (wm * MT * 8 + (lane >> 2)) * PA + (lane & 3);
@@ -143,6 +154,8 @@ __global__ void __launch_bounds__(WM * WN * 32, 2)
       }
     }
   }
+  // the next mode product may start its independent prologue now (it still waits for this grid)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   // epilogue: the output columns (and their eigenvalue sums) depend on (j, h) only
   long long coff[NTW][2];
   double l12[NTW][2];
@@ -185,6 +198,14 @@ __global__ void __launch_bounds__(WM * WN * 32, 2)
   }
 }
 
+static bool pdl_enabled() {  // MFWQ_NO_PDL=1: plain stream-ordered launches (timing experiments)
+  static const int on = [] {
+    const char* e = getenv("MFWQ_NO_PDL");
+    return (e && *e && *e != '0') ? 0 : 1;
+  }();
+  return on != 0;
+}
+
 template <int MT, int WM, int WN, int NTW>
 static void launch(const double* A, int lda, int M, int K, const double* X, ModeView xv, double* C, ModeView cv,
                    long long N, Scale sc, bool kc, cudaStream_t s) {
@@ -202,7 +223,18 @@ static void launch(const double* A, int lda, int M, int K, const double* X, Mode
   dim3 grid((M + BM - 1) / BM, (unsigned)((N + BN - 1) / BN));
   auto go = [&](auto kern) {
     MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, THREADS, smem, s>>>(A, lda, M, K, X, xv, C, cv, N, sc); note_launch();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MFWQ_CUDA(cudaLaunchKernelEx(&cfg, kern, A, lda, M, K, X, xv, C, cv, N, sc));
+    note_launch();
   };
   if (bl == 3) go(modal_kernel<MT, WM, WN, NTW, 3>);
   else if (bl == 2) go(modal_kernel<MT, WM, WN, NTW, 2>);
