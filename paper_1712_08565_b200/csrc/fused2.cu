@@ -702,6 +702,9 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     __syncthreads();
     bside_y(nz0);
   }
+  // everything above reads only x, the operand blocks and the coefficient stage; the output w is
+  // zeroed by the preceding grid (programmatic dependent launch): wait for it before any atomic
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   unsigned parity = 0u;  // phase of the stage mbarrier
 
   // One step over NZ (compile-time) z-elements starting at chunk element el. Phases between the
@@ -985,6 +988,22 @@ void encode_maps(Stiffness& S, Fused2Plan& F) {
 
 void encode_maps(Stiffness& S, Fused2Plan& F);
 
+#ifndef MFWQ_F2_OTF_UNIT
+// w = 0 ahead of the fused kernel's atomics; lets the fused kernel launch at once (its prologue
+// overlaps this pass and it waits with griddepcontrol.wait before the first atomic)
+__global__ void __launch_bounds__(256) f2_zero_out(double* __restrict__ y, long long n) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) y[i] = 0.0;
+}
+void f2_zero_and_chain(double* y, long long n, cudaStream_t s) {
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  f2_zero_out<<<nsm * 4, 256, 0, s>>>(y, n); note_launch();
+}
+#else
+void f2_zero_and_chain(double* y, long long n, cudaStream_t s);
+#endif
+
 template <int P, int NT, bool OTF>
 static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
   constexpr int ZS = f2::zs_for(P, NT);
@@ -1028,9 +1047,19 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   const size_t smem = Smem<P, NT, ZS, OTF>::bytes(F.qe, F.max_chunk);
   auto kern = k_fused<P, NT, ZS, OTF>;
   MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  MFWQ_CUDA(cudaMemsetAsync(y, 0, S.out_elems() * sizeof(double), s));
-  dim3 grid(F.ntile[0] * F.ntile[1], F.ntile[2]);
-  kern<<<grid, NTHR, smem, s>>>(prm, F.maps); note_launch();
+  f2_zero_and_chain(y, (long long)S.out_elems(), s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(F.ntile[0] * F.ntile[1], F.ntile[2]);
+  cfg.blockDim = dim3(NTHR);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MFWQ_CUDA(cudaLaunchKernelEx(&cfg, kern, prm, F.maps));
+  note_launch();
   MFWQ_CUDA(cudaGetLastError());
 }
 
