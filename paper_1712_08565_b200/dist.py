@@ -89,13 +89,17 @@ class SlabPartition:
 
 
 def _exchange(ops_send, ops_recv, group=None):
-    """Post all sends/receives, then wait (works for gloo and NCCL)."""
-    reqs = []
-    for t, peer in ops_recv:
-        reqs.append(dist.irecv(t, src=peer, group=group))
-    for t, peer in ops_send:
-        reqs.append(dist.isend(t, dst=peer, group=group))
-    for q in reqs:
+    """Post all sends/receives of this rank as ONE batch, then wait.
+
+    Under NCCL the batch is a single ncclGroupStart/End, so a rank that both sends to and receives
+    from the same peer (the reverse halo: p rows up, one row down) cannot deadlock on the ordering of
+    separately launched send/recv kernels; gloo runs the ops one by one.  A rank with nothing to
+    exchange posts nothing (never the group's first collective: dist_cg allreduces ||b|| first)."""
+    ops = [dist.P2POp(dist.irecv, t, peer, group=group) for t, peer in ops_recv]
+    ops += [dist.P2POp(dist.isend, t, peer, group=group) for t, peer in ops_send]
+    if not ops:
+        return
+    for q in dist.batch_isend_irecv(ops):
         q.wait()
 
 
