@@ -218,3 +218,47 @@ def test_pcg_c_abi_unaligned_solution_buffer():
     assert rep.iterations == rep_ref.iterations and bool(rep.converged)
     assert relerr(x.cpu().numpy(), u_ref) <= 1e-13
     assert float(buf[0]) == 0.0
+
+
+@pytest.mark.parametrize("p,n_el", [(1, 4), (4, 8), (8, 32)])
+def test_fd_eigenpairs_residual_and_m_orthonormality(p, n_el):
+    """test_solvers.py:14-23 on the device eigensolver (cuSOLVER Dsygvd): K U = M U diag(lam),
+    U^T M U = I to 1e-10, lam > 0."""
+    space = M.tensor_space(p, n_el)
+    P = M.FDPreconditioner(space)
+    K, Mm = P.K1[0], P.M1[0]
+    U, lam = P.U[0], np.asarray(P.lams[0])
+    assert np.abs(K @ U - Mm @ U @ np.diag(lam)).max() <= 1e-10
+    assert np.abs(U.T @ Mm @ U - np.eye(len(lam))).max() <= 1e-10
+    assert lam.min() > 0
+
+
+def test_device_pcg_true_residual_matches_reported():
+    """test_solvers.py:95-102 for the device-resident PCG: the true relative residual of the
+    returned solution is within 10x of the last recursive residual."""
+    space = M.tensor_space(4, 12)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.quarter_ring_map())
+    P = M.FDPreconditioner(space)
+    b = np.random.default_rng(3).standard_normal(space.n_dofs)
+    x, rep = M.cg(A.apply, b, P.apply, tol=1e-10)
+    true_rel = np.linalg.norm(b - A.apply(x)) / np.linalg.norm(b)
+    assert rep.converged and true_rel <= 10 * rep.residuals[-1]
+
+
+def test_preconditioner_robustness_in_p_and_h():
+    """test_acceptance.py:214-232 (criterion 8) on the device path: FD-preconditioned BiCGStab on
+    the oscillating quarter-ring case, iteration counts vary by < 2x across p = 2..8 and h."""
+    geom = M.quarter_ring_map()
+
+    def iters(p, n_el):
+        space = M.tensor_space(p, n_el)
+        A = M.setup_stiffness(space, M.build_tensor_rule(space), geom)
+        rhs = M.assemble_rhs(space, geom, M.oscillating_case().f)
+        _, rep = M.bicgstab(A.apply, rhs, M.FDPreconditioner(space).apply, tol=1e-8)
+        assert rep.converged, (p, n_el)
+        return rep.iterations
+
+    by_p = [iters(p, 16) for p in range(2, 9)]
+    assert max(by_p) < 2 * min(by_p), by_p
+    by_h = [iters(3, n_el) for n_el in (8, 16, 32)]
+    assert max(by_h) < 2 * min(by_h), by_h
