@@ -189,15 +189,23 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
     copy_scalar<<<1, 1, 0, s>>>(rzn, rz); note_launch();
     MFWQ_CUDA(cudaGetLastError());
   };
-  cudaEvent_t ev;
-  MFWQ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  double* hsc = nullptr;
-  MFWQ_CUDA(cudaMallocHost(&hsc, 2 * sizeof(double)));
-  struct Cleanup {
-    cudaEvent_t e;
-    double* h;
-    ~Cleanup() { cudaEventDestroy(e); cudaFreeHost(h); }
-  } cleanup{ev, hsc};
+  // pinned landing slot for the two scalars and the event marking their arrival: created once per
+  // host thread (cudaMallocHost costs ~1 ms, far more than a small solve)
+  struct ScalarSlot {
+    cudaEvent_t ev = nullptr;
+    double* h = nullptr;
+    ~ScalarSlot() {
+      if (ev) cudaEventDestroy(ev);
+      if (h) cudaFreeHost(h);
+    }
+  };
+  static thread_local ScalarSlot slot;
+  if (!slot.h) {
+    MFWQ_CUDA(cudaEventCreateWithFlags(&slot.ev, cudaEventDisableTiming));
+    MFWQ_CUDA(cudaMallocHost(&slot.h, 2 * sizeof(double)));
+  }
+  cudaEvent_t ev = slot.ev;
+  double* hsc = slot.h;
   for (int k = 1; k <= maxit; ++k) {
     A.apply(p, Ap, s);
     out.matvecs++;
