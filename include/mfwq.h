@@ -15,6 +15,7 @@
  *   mfwq_stiffness_create  StiffnessOperator.__init__ / setup_stiffness operators.py:138-163, 227
  *   mfwq_stiffness_set_*   _eval_stiffness_coeffs                      operators.py:64-84
  *   mfwq_stiffness_apply   StiffnessOperator.apply                     operators.py:185-204
+ *   mfwq_stiffness_apply_host / _host_join  (same, host buffers, pipelined)  operators.py:185-204
  *   mfwq_stiffness_flops   CostMeter count of one apply                kron.py:90-96, operators.py:199-203
  *   mfwq_fd_create         FDPreconditioner.__init__                   solvers.py:72-101
  *   mfwq_fd_apply          FDPreconditioner.apply                      solvers.py:107-115
@@ -110,6 +111,14 @@ int mfwq_stiffness_get_coeff(mfwq_stiffness_t h, int key, double* out_dev, void*
 int mfwq_stiffness_sizes(mfwq_stiffness_t h, int* n3, int* m3, long long* N, long long* Nq);
 /* y = K x  (device pointers, length N); y is overwritten */
 int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x_dev, double* y_dev, void* stream);
+/* y_host = K x_host with HOST buffers (pinned for full overlap), asynchronous: H2D on the handle's
+   copy stream into one of two device staging buffers, the kernel on `stream`, D2H on the handle's
+   second copy stream.  Consecutive calls (on any handles) overlap both copy directions and the
+   kernels; y_host is valid after mfwq_stiffness_host_join(h, stream) + a sync of `stream`.
+   (operators.py:185-204 with numpy in / numpy out, as a streaming pipeline) */
+int mfwq_stiffness_apply_host(mfwq_stiffness_t h, const double* x_host, double* y_host, void* stream);
+/* make `stream` wait for every outstanding D2H of h's host pipeline */
+int mfwq_stiffness_host_join(mfwq_stiffness_t h, void* stream);
 /* Multi-GPU slab: restrict the operator to z-elements [e_lo, e_hi).
    Must precede set_geometry/set_coeffs (only the slab's quadrature planes are stored).
    apply() then maps the input window of interior DoF planes [v_lo, v_hi) to the

@@ -8,7 +8,30 @@
 using namespace mfwq;
 
 struct mfwq_rule1d_s { Rule1D r; int nfun; };
-struct mfwq_stiffness_s { Stiffness op; };
+// host-buffer pipeline state (mfwq_stiffness_apply_host): two device staging pairs, one H2D and one
+// D2H stream, and the events that order staging reuse; created on first use
+struct HostPipe {
+  bool ready = false;
+  int i = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  DevBuf<double> x[2], y[2];
+  cudaEvent_t landed[2] = {}, freed[2] = {}, read[2] = {};
+  bool freed_set[2] = {false, false}, read_set[2] = {false, false};
+  ~HostPipe() {
+    if (!ready) return;
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(landed[k]);
+      cudaEventDestroy(freed[k]);
+      cudaEventDestroy(read[k]);
+    }
+    cudaStreamDestroy(h2d);
+    cudaStreamDestroy(d2h);
+  }
+};
+struct mfwq_stiffness_s {
+  Stiffness op;
+  HostPipe pipe;
+};
 struct mfwq_fd_s { FastDiag fd; };
 struct mfwq_quad_s { Quadrature q; };
 
@@ -168,6 +191,52 @@ int mfwq_stiffness_sizes(mfwq_stiffness_t h, int* n3, int* m3, long long* N, lon
 
 int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x, double* y, void* stream) {
   return guard([&] { h->op.apply(x, y, (cudaStream_t)stream); });
+}
+
+int mfwq_stiffness_apply_host(mfwq_stiffness_t h, const double* x_host, double* y_host, void* stream) {
+  return guard([&] {
+    HostPipe& P = h->pipe;
+    Stiffness& S = h->op;
+    const size_t nin = S.in_elems(), nout = S.out_elems();
+    if (!P.ready) {
+      MFWQ_CUDA(cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking));
+      MFWQ_CUDA(cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        P.x[k].alloc(nin);
+        P.y[k].alloc(nout);
+        MFWQ_CUDA(cudaEventCreateWithFlags(&P.landed[k], cudaEventDisableTiming));
+        MFWQ_CUDA(cudaEventCreateWithFlags(&P.freed[k], cudaEventDisableTiming));
+        MFWQ_CUDA(cudaEventCreateWithFlags(&P.read[k], cudaEventDisableTiming));
+      }
+      P.ready = true;
+    }
+    const cudaStream_t s = (cudaStream_t)stream;
+    const int i = P.i;
+    P.i ^= 1;
+    // H2D into staging pair i once the kernel that last read it is done
+    if (P.freed_set[i]) MFWQ_CUDA(cudaStreamWaitEvent(P.h2d, P.freed[i], 0));
+    MFWQ_CUDA(cudaMemcpyAsync(P.x[i].ptr, x_host, nin * sizeof(double), cudaMemcpyHostToDevice, P.h2d));
+    MFWQ_CUDA(cudaEventRecord(P.landed[i], P.h2d));
+    // the kernel on the caller's stream: after its input landed and the D2H that last read y[i]
+    MFWQ_CUDA(cudaStreamWaitEvent(s, P.landed[i], 0));
+    if (P.read_set[i]) MFWQ_CUDA(cudaStreamWaitEvent(s, P.read[i], 0));
+    S.apply(P.x[i].ptr, P.y[i].ptr, s);
+    MFWQ_CUDA(cudaEventRecord(P.freed[i], s));
+    P.freed_set[i] = true;
+    // D2H of the result on the D2H stream
+    MFWQ_CUDA(cudaStreamWaitEvent(P.d2h, P.freed[i], 0));
+    MFWQ_CUDA(cudaMemcpyAsync(y_host, P.y[i].ptr, nout * sizeof(double), cudaMemcpyDeviceToHost, P.d2h));
+    MFWQ_CUDA(cudaEventRecord(P.read[i], P.d2h));
+    P.read_set[i] = true;
+  });
+}
+
+int mfwq_stiffness_host_join(mfwq_stiffness_t h, void* stream) {
+  return guard([&] {
+    HostPipe& P = h->pipe;
+    for (int k = 0; k < 2; ++k)
+      if (P.read_set[k]) MFWQ_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, P.read[k], 0));
+  });
 }
 
 int mfwq_stiffness_set_slab(mfwq_stiffness_t h, int e_lo, int e_hi) {

@@ -65,6 +65,10 @@ def _create_handle(rule, n_dofs):
     return h, tuple(int(v) for v in n3), tuple(int(v) for v in m3), Nq.value
 
 
+
+_COPY_STREAMS = {}  # device -> (H2D stream, D2H stream) for the pinned-host apply paths
+_JOIN_STREAMS = {}  # device -> stream that only waits for host-pipeline D2H copies (completion events)
+
 class StiffnessOperator:
     """Matrix-free weighted-quadrature stiffness operator (interior space)."""
 
@@ -213,7 +217,31 @@ class StiffnessOperator:
         ``event`` has completed (``event.synchronize()`` or ``torch.cuda.synchronize()``)."""
         if not _dev.is_pinned_host(v):
             raise ValueError("apply_pipelined takes a pinned host torch tensor")
-        return self._apply_pinned(v, meter, out, d2h_side=True)
+        torch = _dev.torch
+        if v.numel() != self._in_len:
+            raise ValueError(f"expected vector of length {self._in_len}, got {v.numel()}")
+        o = out if out is not None else torch.empty(self._out_len, dtype=torch.float64, pin_memory=True)
+        if o.numel() != self._out_len or o.is_cuda or o.dtype != torch.float64 or not o.is_contiguous():
+            raise ValueError("out must be a contiguous float64 host tensor of the output length")
+        x = v.reshape(-1)
+        if x.dtype != torch.float64 or not x.is_contiguous():
+            x = x.to(torch.float64).contiguous().pin_memory()
+        cur = torch.cuda.current_stream()
+        # native pipeline (mfwq_stiffness_apply_host): H2D / kernel / D2H on three streams, two device
+        # staging pairs per operator; no per-call Python stream or event objects
+        _lib.check(_lib.lib().mfwq_stiffness_apply_host(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(o.data_ptr()),
+                                                        C.c_void_p(cur.cuda_stream)))
+        dev = torch.cuda.current_device()
+        if dev not in _JOIN_STREAMS:
+            _JOIN_STREAMS[dev] = torch.cuda.Stream()
+        js = _JOIN_STREAMS[dev]
+        _lib.check(_lib.lib().mfwq_stiffness_host_join(self._h, C.c_void_p(js.cuda_stream)))
+        done = torch.cuda.Event()
+        done.record(js)
+        self._host_keep = (x, o)  # host buffers stay referenced while their copies are in flight
+        if meter is not None:
+            meter.add_flops(self.apply_flops)
+        return o, done
 
     def _apply_pinned(self, v, meter, out, d2h_side=False):
         """Pinned host torch tensor in, pinned host tensor out, asynchronous like torch's non_blocking
@@ -225,7 +253,13 @@ class StiffnessOperator:
             raise ValueError(f"expected vector of length {self._in_len}, got {v.numel()}")
         st = getattr(self, "_pipe", None)
         if st is None:
-            st = self._pipe = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
+            # one H2D and one D2H side stream per device, shared by all operators: consecutive calls on
+            # different operators then form a single in-order copy pipeline in each direction
+            dev = torch.cuda.current_device()
+            if dev not in _COPY_STREAMS:
+                _COPY_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+            h2d_s, d2h_s = _COPY_STREAMS[dev]
+            st = self._pipe = {"h2d": h2d_s, "d2h": d2h_s,
                                "x": [_dev.empty(self._in_len) for _ in range(2)],
                                "y": [_dev.empty(self._out_len) for _ in range(2)], "free": [None, None],
                                "read": [None, None], "i": 0}
