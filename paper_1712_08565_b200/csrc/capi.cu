@@ -190,7 +190,12 @@ int mfwq_stiffness_sizes(mfwq_stiffness_t h, int* n3, int* m3, long long* N, lon
 }
 
 int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x, double* y, void* stream) {
-  return guard([&] { h->op.apply(x, y, (cudaStream_t)stream); });
+  return guard([&] {
+    // the output is zeroed before the kernel reads x: an overlapping (in-place) call is rejected
+    const double *x1 = x + h->op.in_elems(), *y1 = y + h->op.out_elems();
+    if (x < y1 && y < x1) throw ValueErr("x and y must not overlap (y is overwritten before x is read)");
+    h->op.apply(x, y, (cudaStream_t)stream);
+  });
 }
 
 int mfwq_stiffness_apply_host(mfwq_stiffness_t h, const double* x_host, double* y_host, void* stream) {

@@ -262,3 +262,16 @@ def test_preconditioner_robustness_in_p_and_h():
     assert max(by_p) < 2 * min(by_p), by_p
     by_h = [iters(3, n_el) for n_el in (8, 16, 32)]
     assert max(by_h) < 2 * min(by_h), by_h
+
+
+def test_in_place_apply_rejected():
+    """y is zeroed before the fused kernel reads x, so an overlapping out= must raise, not corrupt."""
+    import torch
+
+    space = M.tensor_space(2, 4)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), M.identity_map(3))
+    x = torch.ones(space.n_dofs, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        A.apply(x, out=x)
+    y = A.apply(x)
+    assert float(torch.linalg.vector_norm(y)) > 0
