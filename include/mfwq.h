@@ -55,6 +55,17 @@ long long mfwq_launch_count(void);
 
 /* ---------------- 1D weighted-quadrature rule (host) ---------------- */
 typedef struct mfwq_rule1d_s* mfwq_rule1d_t;
+/* Register the LAPACK whose dgelsd (ILP64: 64-bit integers, Fortran convention) solves the
+   per-row min-norm least-squares systems of the WQ weights, the driver np.linalg.lstsq calls
+   (wq.py:86-99).  lib_path: a shared library (dlopen'ed); symbol: its dgelsd (numpy's bundled
+   OpenBLAS exports "scipy_dgelsd_64_"); its dsyevd (same name with "syevd") also builds the
+   Gauss-Legendre rules the way numpy.polynomial.legendre.leggauss does (wq.py:41-49, the exact
+   Gram right-hand sides).  With the host's numpy LAPACK the weights are the reference's bit for
+   bit; with none registered a built-in Jacobi SVD solves the rows (same
+   truncation rule).  MFWQ_E_VALUE if the library or symbol cannot be loaded. */
+int mfwq_set_lapack(const char* lib_path, const char* symbol);
+/* 1 when a LAPACK dgelsd is registered, else 0 */
+int mfwq_lapack_active(void);
 /* knots: open knot vector of degree p on [0,1] (splines.py:16-49) */
 int mfwq_rule1d_build(int p, int nknots, const double* knots, mfwq_rule1d_t* out);
 /* npts, nfun, boundary extra used, nnz[6] of W00,W01,W10,W11 (nfun x npts), B0,B1 (npts x nfun) */
@@ -84,7 +95,8 @@ typedef struct {
 int mfwq_stiffness_create(const mfwq_stiffness_desc* d, mfwq_stiffness_t* out);
 /* kind: MFWQ_GEOM_*; affine9: row-major A for AFFINE; K9: constant diffusion
    (NULL = identity); J_dev: device (Nq,3,3) for JACOBIAN; Kfield_dev: device
-   (Nq,3,3) per-point diffusion or NULL.  Raises MFWQ_E_DEGENERATE if det J <= 0. */
+   (Nq,3,3) per-point diffusion or NULL.  Both are FULL-domain arrays (all m3 quadrature planes),
+   also on slab handles, which read their own planes [q_lo, q_hi) from them.  Raises MFWQ_E_DEGENERATE if det J <= 0. */
 int mfwq_stiffness_set_geometry(mfwq_stiffness_t h, int kind, const double* affine9, const double* K9,
                                 const double* J_dev, const double* Kfield_dev, void* stream);
 /* on-the-fly coefficients (operators.py:138, 171-183, 207-220: on_the_fly=True): no N_q grids are
@@ -126,9 +138,11 @@ int mfwq_stiffness_host_join(mfwq_stiffness_t h, void* stream);
 int mfwq_stiffness_set_slab(mfwq_stiffness_t h, int e_lo, int e_hi);
 /* info6 = {e_lo, e_hi, v_lo, v_hi, y_lo, y_hi} */
 int mfwq_stiffness_slab_info(mfwq_stiffness_t h, int* info6);
-/* select kernel path: 0 = auto (fused v2), 1 = generic K1 composition, 2 = fused v2, 3 = fused v1 */
+/* select kernel path: 0 = auto (fused), 1 = generic K1 composition, 2 = fused */
 int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path);
-int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* stencil_ok, double* stencil_dev);
+/* term_mask: bit 3a+b set when C_ab is not identically zero; fused_ok: the rule fits the fused
+   kernel's element-blocked structure; kernel_terms: term class the fused kernel runs (3, 5 or 9) */
+int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* fused_ok, int* kernel_terms);
 int mfwq_stiffness_flops(mfwq_stiffness_t h, long long* flops);
 /* same count restricted to the terms with a non-zero coefficient grid (what the kernels execute) */
 int mfwq_stiffness_flops_active(mfwq_stiffness_t h, long long* flops);

@@ -47,6 +47,16 @@ def to_device(v, n=None):
     return t, host
 
 
+def check_out(out, n):
+    """Validate a caller-provided output buffer before its pointer reaches a kernel."""
+    if not (is_device_tensor(out) and out.dtype == torch.float64 and out.is_contiguous()
+            and out.numel() == int(n)):
+        raise ValueError(f"out must be a contiguous float64 CUDA tensor of length {int(n)}")
+    if out.device.index != torch.cuda.current_device():
+        raise ValueError("out must live on the current CUDA device")
+    return out
+
+
 def empty(n):
     require_cuda()
     return torch.empty(int(n), dtype=torch.float64, device="cuda")

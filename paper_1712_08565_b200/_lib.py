@@ -37,6 +37,8 @@ _SIGS = {
     "mfwq_last_error": (C.c_char_p, []),
     "mfwq_version": (C.c_int, []),
     "mfwq_launch_count": (C.c_longlong, []),
+    "mfwq_set_lapack": (C.c_int, [C.c_char_p, C.c_char_p]),
+    "mfwq_lapack_active": (C.c_int, []),
     "mfwq_rule1d_build": (C.c_int, [C.c_int, C.c_int, dp, C.POINTER(C.c_void_p)]),
     "mfwq_rule1d_sizes": (C.c_int, [C.c_void_p, ip, ip, ip, ip]),
     "mfwq_rule1d_export": (C.c_int, [C.c_void_p, dp, C.POINTER(ip), C.POINTER(ip), C.POINTER(dp)]),
@@ -57,7 +59,7 @@ _SIGS = {
     "mfwq_stiffness_set_path": (C.c_int, [C.c_void_p, C.c_int]),
     "mfwq_stiffness_set_slab": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "mfwq_stiffness_slab_info": (C.c_int, [C.c_void_p, ip]),
-    "mfwq_stiffness_info": (C.c_int, [C.c_void_p, ip, ip, dp]),
+    "mfwq_stiffness_info": (C.c_int, [C.c_void_p, ip, ip, ip]),
     "mfwq_stiffness_flops": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "mfwq_stiffness_flops_active": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "mfwq_stiffness_destroy": (None, [C.c_void_p]),
@@ -104,7 +106,29 @@ def lib():
             f.restype = res
             f.argtypes = args
         _lib = h
+        _register_lapack(h)
     return _lib
+
+
+def numpy_lapack():
+    """(library path, dgelsd symbol) of the LAPACK numpy's own ``np.linalg.lstsq`` calls, i.e. the
+    driver the reference's WQ rows are solved with (wq.py:97), or None if it cannot be found."""
+    import glob
+    libs = os.path.join(os.path.dirname(os.path.dirname(np.__file__)), "numpy.libs")
+    for pat in ("libscipy_openblas64_*.so*",):
+        for path in sorted(glob.glob(os.path.join(libs, pat))):
+            return path, "scipy_dgelsd_64_"
+    return None
+
+
+def _register_lapack(h):
+    """Point the native WQ rule builder at numpy's dgelsd (bit-identical weights to the
+    reference); MFWQ_NO_NUMPY_LAPACK=1 keeps the built-in Jacobi SVD (tests of that path)."""
+    if os.environ.get("MFWQ_NO_NUMPY_LAPACK") == "1":
+        return
+    found = numpy_lapack()
+    if found is not None:
+        h.mfwq_set_lapack(found[0].encode(), found[1].encode())  # best effort: falls back to Jacobi
 
 
 _CODES = {1: ValueError, 2: WQConstructionError, 3: DegenerateGeometryError, 4: EigenSolveError,

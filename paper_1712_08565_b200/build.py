@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC] + os.environ.get("MFWQ_NVCC_EXTRA", "").split()
-SOURCES = ["rule1d.cpp", "stiffness.cu", "fused_matvec.cu", "fused2.cu", "fused2_otf.cu", "fd.cu", "modal_gemm.cu", "pcg.cu",
+SOURCES = ["rule1d.cpp", "stiffness.cu", "fused2.cu", "fused2_otf.cu", "fd.cu", "modal_gemm.cu", "pcg.cu",
            "bicgstab.cu", "quadrature.cu", "capi.cu"]
 LIBS = ["-lcusolver", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64"]
 

@@ -1,4 +1,6 @@
 // extern "C" boundary of libmfwq.so (declared in include/mfwq.h).
+#include <dlfcn.h>
+
 #include <cstring>
 #include <string>
 
@@ -76,6 +78,26 @@ extern "C" {
 const char* mfwq_last_error(void) { return g_err.c_str(); }
 int mfwq_version(void) { return 1; }
 long long mfwq_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int mfwq_set_lapack(const char* lib_path, const char* symbol) {
+  return guard([&] {
+    if (!lib_path || !symbol) throw ValueErr("mfwq_set_lapack: library path and symbol required");
+    void* h = dlopen(lib_path, RTLD_NOW | RTLD_LOCAL);  // kept open for the life of the process
+    if (!h) throw ValueErr(std::string("cannot load LAPACK library: ") + dlerror());
+    void* fn = dlsym(h, symbol);
+    if (!fn) throw ValueErr(std::string("LAPACK library has no symbol ") + symbol);
+    // the companion dsyevd (np.linalg.eigvalsh, behind numpy's Gauss-Legendre rule): same naming
+    std::string ev(symbol);
+    const size_t at = ev.find("gelsd");
+    if (at == std::string::npos) throw ValueErr("symbol must name a dgelsd (e.g. scipy_dgelsd_64_)");
+    ev.replace(at, 5, "syevd");
+    void* fe = dlsym(h, ev.c_str());
+    if (!fe) throw ValueErr("LAPACK library has no symbol " + ev);
+    set_lapack(reinterpret_cast<dgelsd64_t>(fn), reinterpret_cast<dsyevd64_t>(fe));
+  });
+}
+
+int mfwq_lapack_active(void) { return have_dgelsd() ? 1 : 0; }
 
 int mfwq_rule1d_build(int p, int nknots, const double* knots, mfwq_rule1d_t* out) {
   return guard([&] {
@@ -215,6 +237,16 @@ int mfwq_stiffness_apply_host(mfwq_stiffness_t h, const double* x_host, double* 
       }
       P.ready = true;
     }
+    if (P.x[0].n < nin || P.y[0].n < nout) {
+      // the slab window grew since the staging pairs were sized (mfwq_stiffness_set_slab): drain the
+      // pipe, then resize both pairs
+      for (int k = 0; k < 2; ++k) {
+        if (P.read_set[k]) MFWQ_CUDA(cudaEventSynchronize(P.read[k]));
+        if (P.freed_set[k]) MFWQ_CUDA(cudaEventSynchronize(P.freed[k]));
+        P.x[k].alloc(nin);
+        P.y[k].alloc(nout);
+      }
+    }
     const cudaStream_t s = (cudaStream_t)stream;
     const int i = P.i;
     P.i ^= 1;
@@ -258,16 +290,17 @@ int mfwq_stiffness_slab_info(mfwq_stiffness_t h, int* info6) {
 
 int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path) {
   return guard([&] {
-    if (path < 0 || path > 3) throw ValueErr("path must be 0..3");
+    if (path < 0 || path > 2) throw ValueErr("path must be 0..2");
     h->op.path = path;
   });
 }
 
-int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* stencil_ok, double* stencil_dev) {
+int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* fused_ok, int* kernel_terms) {
   return guard([&] {
-    *term_mask = h->op.term_mask();
-    *stencil_ok = h->op.stencil.ok ? 1 : 0;
-    *stencil_dev = h->op.stencil.max_dev;
+    const int tm = h->op.term_mask();
+    *term_mask = tm;
+    *fused_ok = fused2_accepts(h->op) ? 1 : 0;
+    *kernel_terms = (tm & ~0x111) == 0 ? 3 : ((tm & ~0x11B) == 0 ? 5 : 9);
   });
 }
 
@@ -316,6 +349,7 @@ void mfwq_fd_destroy(mfwq_fd_t h) { delete h; }
 int mfwq_pcg_solve(mfwq_stiffness_t A, mfwq_fd_t P, const double* b, double* x, double tol, int maxit,
                    double* residuals, mfwq_krylov_report* rep, void* stream) {
   return guard([&] {
+    if (A->op.is_slab()) throw ValueErr("mfwq_pcg_solve takes a whole-domain operator (slab handles: mfwq_pcg_solve_comm)");
     std::vector<double> hist;
     KrylovOut o;
     pcg_solve(A->op, P ? &P->fd : nullptr, b, x, A->op.N, tol, maxit, hist, o, (cudaStream_t)stream);

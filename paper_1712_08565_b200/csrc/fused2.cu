@@ -816,9 +816,43 @@ struct Fused2Plan {
   f2::Maps maps;  // 16 x 16 x 4 / x 2 boxes: the ZS x 2 planes of a regular step
 };
 
-bool build_elem_tables(const Dir1D& d, std::vector<double>& B, std::vector<double>& W, std::vector<int>& eq);
-
 #ifndef MFWQ_F2_OTF_UNIT  // plan + tensor maps: defined once (fused2.cu), not in fused2_otf.cu
+// Element-blocked 1D tables from the operator's banded factors (every non-zero of the reference's
+// CSR factors must fall inside the element block; false = the rule is outside this structure)
+bool build_elem_tables(const Dir1D& d, std::vector<double>& B, std::vector<double>& W, std::vector<int>& eq) {
+  const int p = d.p, NB = p + 1, NW = p + 2, m = d.m;
+  eq.assign(m, 0);
+  for (int e = 0; e < d.n_el; ++e)
+    for (int q = d.elem_q0[e]; q < d.elem_q0[e + 1]; ++q) eq[q] = e;
+  B.assign(size_t(2) * m * NB, 0.0);
+  W.assign(size_t(4) * m * NW, 0.0);
+  // B band: interior column c <-> full j = c+1 ; k = j - e(q)
+  for (int b = 0; b < 2; ++b) {
+    const BandHost& h = d.B[b].h;
+    for (int q = 0; q < m; ++q)
+      for (int u = 0; u < h.width; ++u) {
+        double v = h.vals[size_t(q) * h.width + u];
+        if (v == 0.0) continue;
+        int j = h.start[q] + u + 1, k = j - eq[q];
+        if (k < 0 || k >= NB) return false;
+        B[(size_t(b) * m + q) * NB + k] = v;
+      }
+  }
+  // W band: interior row i <-> full j = i+1 ; k = j - e(q) + 1
+  for (int w = 0; w < 4; ++w) {
+    const BandHost& h = d.W[w].h;
+    for (int i = 0; i < h.rows; ++i)
+      for (int u = 0; u < h.width; ++u) {
+        double v = h.vals[size_t(i) * h.width + u];
+        if (v == 0.0) continue;
+        int q = h.start[i] + u, j = i + 1, k = j - eq[q] + 1;
+        if (k < 0 || k >= NW) return false;
+        W[(size_t(w) * m + q) * NW + k] = v;
+      }
+  }
+  return true;
+}
+
 static std::vector<f2::Tile> f2_tiles_inplane(const Dir1D& d) {
   // greedy element-aligned tiles of <= 16 quadrature points from element 0: with an even
   // number of boundary extras every tile but the last is exactly 16 points wide, so the
@@ -1102,6 +1136,14 @@ bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s) {
   if (!F->ok) return false;
   if (S.otf) return fused2_apply_otf(S, *F, x, y, s);
   return dispatch_p<false>(S, *F, x, y, s);
+}
+
+bool fused2_accepts(Stiffness& S) { return fused2_plan(S)->ok; }
+
+void Stiffness::apply_fused(const double* x, double* y, cudaStream_t s) {
+  if (fused2_apply(*this, x, y, s)) return;
+  if (is_slab()) throw NotImplErr("slab operators need the element-blocked fused kernel (p <= 10, n_el >= 2)");
+  apply_generic(x, y, s);  // rule outside the element-blocked structure: composed K1 path (still GPU)
 }
 #else
 bool fused2_apply_otf(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {

@@ -24,12 +24,6 @@ struct Dir1D {
   DevBuf<double> pts_d;
 };
 
-// Interior-tile stencil description (uniform knots; see fused kernel).
-struct StencilInfo {
-  bool ok = false;
-  double max_dev = 0.0;
-};
-
 class Stiffness {
  public:
   Dir1D dir[3];
@@ -39,9 +33,8 @@ class Stiffness {
   bool grid_nonzero[6] = {true, true, true, true, true, true};
   bool coeffs_ready = false;
   long long flops = 0;            // CostMeter count of one apply (kron.py:90-96)
-  int path = 0;                   // 0 = auto/fused v2, 1 = generic (K1), 2 = fused v2, 3 = fused v1
-  StencilInfo stencil;
-  std::shared_ptr<void> fused_plan, fused2_plan;  // element-blocked tables + tiles of the fused kernel
+  int path = 0;                   // 0 = auto (fused), 1 = generic (K1 composition), 2 = fused
+  std::shared_ptr<void> fused2_plan;  // element-blocked tables + tiles of the fused kernel
   long long nnz_[3][6] = {};      // interior-restricted nnz per direction: B0,B1,W00,W01,W10,W11
 
   // slab (multi-GPU) window, global indices: local z-elements [e_lo, e_hi), input planes
@@ -96,7 +89,6 @@ class Stiffness {
  private:
   void compute_flops();
   void detect_nonzero(cudaStream_t s);
-  void analyse_stencil();
 };
 
 class FastDiag {
@@ -124,6 +116,7 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
 
 // element-blocked fused matvec (fused2.cu); false when the rule is outside its structure
 bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s);
+bool fused2_accepts(Stiffness& S);  // the rule fits the element-blocked structure (plans it)
 
 void kron_apply_dense(int d, const int* rows, const int* cols, const double* const* A, const double* x, double* y,
                       int accumulate, cudaStream_t s);

@@ -191,20 +191,24 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
   };
   // pinned landing slot for the two scalars and the event marking their arrival: created once per
   // host thread (cudaMallocHost costs ~1 ms, far more than a small solve)
+  // host thread; the event belongs to a device, so there is one per device the thread solves on
+  constexpr int MAXDEV = 64;
   struct ScalarSlot {
-    cudaEvent_t ev = nullptr;
+    cudaEvent_t ev[64] = {};
     double* h = nullptr;
     ~ScalarSlot() {
-      if (ev) cudaEventDestroy(ev);
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
       if (h) cudaFreeHost(h);
     }
   };
   static thread_local ScalarSlot slot;
-  if (!slot.h) {
-    MFWQ_CUDA(cudaEventCreateWithFlags(&slot.ev, cudaEventDisableTiming));
-    MFWQ_CUDA(cudaMallocHost(&slot.h, 2 * sizeof(double)));
-  }
-  cudaEvent_t ev = slot.ev;
+  int cur_dev = 0;
+  MFWQ_CUDA(cudaGetDevice(&cur_dev));
+  if (cur_dev < 0 || cur_dev >= MAXDEV) throw ValueErr("device index out of range");
+  if (!slot.h) MFWQ_CUDA(cudaMallocHost(&slot.h, 2 * sizeof(double)));
+  if (!slot.ev[cur_dev]) MFWQ_CUDA(cudaEventCreateWithFlags(&slot.ev[cur_dev], cudaEventDisableTiming));
+  cudaEvent_t ev = slot.ev[cur_dev];
   double* hsc = slot.h;
   for (int k = 1; k <= maxit; ++k) {
     A.apply(p, Ap, s);

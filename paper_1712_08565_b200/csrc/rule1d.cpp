@@ -5,8 +5,9 @@
 //   wq.py:41-164       (Gauss rule, exact Gram, WQ points, per-row min-norm
 //                       least-squares weights, boundary-point retry loop)
 //   solvers.py:48-62   (exact interior 1D stiffness/mass for FD)
-// Min-norm least squares uses a one-sided Jacobi SVD with numpy's default
-// truncation (rcond = eps * max(rows, cols)), matching np.linalg.lstsq.
+// Min-norm least squares: LAPACK dgelsd with np.linalg.lstsq's calling sequence when the host
+// process registers a LAPACK (mfwq_set_lapack), else a one-sided Jacobi SVD with numpy's default
+// truncation (rcond = eps * max(rows, cols)).
 #include "rule1d.h"
 
 #include <algorithm>
@@ -97,8 +98,109 @@ Csr collocation(const Knots& kv, const std::vector<double>& x, int deriv) {
   return A;
 }
 
-// Gauss-Legendre on [-1,1] by Newton on P_n (numpy.polynomial.legendre.leggauss)
+// numpy's pairwise summation of a contiguous double array (np.sum; numpy/_core loops_utils):
+// fewer than 8 values sequentially from -0.0, up to 128 in eight interleaved partial sums
+static double np_pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = -0.0;
+    for (int i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += a[i];
+  return res;
+}
+
+// numpy.polynomial.legendre.legval for the coefficient vector c (length nc), Clenshaw form
+static double np_legval(double x, const double* c, int nc) {
+  if (nc == 1) return c[0] + 0.0 * x;
+  if (nc == 2) return c[0] + c[1] * x;
+  int nd = nc;
+  double c0 = c[nc - 2], c1 = c[nc - 1];
+  for (int i = 3; i <= nc; ++i) {
+    const double tmp = c0;
+    nd = nd - 1;
+    c0 = c[nc - i] - c1 * (double(nd - 1) / double(nd));
+    c1 = tmp + c1 * x * (double(2 * nd - 1) / double(nd));
+  }
+  return c0 + c1 * x;
+}
+
+// numpy.polynomial.legendre.leggauss, operation for operation: eigenvalues of the scaled
+// companion matrix (LAPACK dsyevd, as np.linalg.eigvalsh), one Newton step, weights from
+// L_{n-1} and L_n' (the latter at the unrefined roots), symmetrised and scaled by 2 / np.sum.
+// The reference's Gauss rules (wq.py:41-49) come from it, so the exact Gram matrices and with
+// them the WQ right-hand sides are bit-identical.
+static dsyevd64_t g_dsyevd = nullptr;
+static bool leggauss_numpy(int n, std::vector<double>& z, std::vector<double>& w) {
+  if (!g_dsyevd) return false;
+  if (n == 1) {
+    z.assign(1, 0.0);
+    w.assign(1, 2.0);
+    return true;
+  }
+  typedef long long i64;
+  std::vector<double> mat(size_t(n) * n, 0.0), scl(n), x(n);
+  for (int k = 0; k < n; ++k) scl[k] = 1.0 / std::sqrt(double(2 * k + 1));
+  for (int k = 1; k < n; ++k) mat[size_t(k - 1) * n + k] = mat[size_t(k) * n + k - 1] = double(k) * scl[k - 1] * scl[k];
+  {  // np.linalg.eigvalsh(m) (UPLO='L', workspace query first); m is symmetric
+    const char jobz = 'N', uplo = 'L';
+    i64 N = n, lda = n, lwork = -1, liwork = -1, info = 0, iwq = 0;
+    double wq = 0.0;
+    g_dsyevd(&jobz, &uplo, &N, mat.data(), &lda, x.data(), &wq, &lwork, &iwq, &liwork, &info, 1, 1);
+    if (info != 0) return false;
+    lwork = i64(wq);
+    liwork = iwq;
+    std::vector<double> work(size_t(std::max<i64>(lwork, 1)));
+    std::vector<i64> iwork(size_t(std::max<i64>(liwork, 1)));
+    g_dsyevd(&jobz, &uplo, &N, mat.data(), &lda, x.data(), work.data(), &lwork, iwork.data(), &liwork, &info, 1, 1);
+    if (info != 0) return false;
+  }
+  std::vector<double> c(n + 1, 0.0), der(n), cc(n + 1);
+  c[n] = 1.0;
+  cc = c;  // legder(c): derivative coefficients
+  for (int j = n; j > 2; --j) {
+    der[j - 1] = double(2 * j - 1) * cc[j];
+    cc[j - 2] += cc[j];
+  }
+  if (n > 1) der[1] = 3.0 * cc[2];
+  der[0] = cc[1];
+  std::vector<double> dy(n), df(n), fm(n), ww(n);
+  for (int k = 0; k < n; ++k) {
+    dy[k] = np_legval(x[k], c.data(), n + 1);
+    df[k] = np_legval(x[k], der.data(), n);
+  }
+  for (int k = 0; k < n; ++k) x[k] -= dy[k] / df[k];
+  double fmax = 0.0, dmax = 0.0;
+  for (int k = 0; k < n; ++k) {
+    fm[k] = np_legval(x[k], c.data() + 1, n);
+    fmax = std::max(fmax, std::fabs(fm[k]));
+    dmax = std::max(dmax, std::fabs(df[k]));
+  }
+  for (int k = 0; k < n; ++k) {
+    fm[k] /= fmax;
+    df[k] /= dmax;
+    ww[k] = 1.0 / (fm[k] * df[k]);
+  }
+  z.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int k = 0; k < n; ++k) {
+    w[k] = (ww[k] + ww[n - 1 - k]) / 2.0;
+    z[k] = (x[k] - x[n - 1 - k]) / 2.0;
+  }
+  const double f = 2.0 / np_pairwise_sum(w.data(), n);
+  for (int k = 0; k < n; ++k) w[k] *= f;
+  return true;
+}
+
+// Gauss-Legendre on [-1,1]: numpy's leggauss when a LAPACK is registered, else Newton on P_n
 static void legendre(int n, std::vector<double>& z, std::vector<double>& w) {
+  if (leggauss_numpy(n, z, w)) return;
   z.assign(n, 0.0);
   w.assign(n, 0.0);
   for (int i = 0; i < n; ++i) {
@@ -173,9 +275,49 @@ std::vector<double> wq_points(const Knots& kv, int extra) {
   return out;
 }
 
+// LAPACK dgelsd (ILP64 interface), the driver np.linalg.lstsq calls (wq.py:97).  When the host
+// process provides one (mfwq_set_lapack: numpy's own bundled LAPACK), the rows are solved by it
+// with numpy's exact calling sequence, so the weights are the reference's bit for bit; otherwise
+// the self-contained Jacobi SVD below is used (same truncation rule, conditioning-limited agreement).
+static dgelsd64_t g_dgelsd = nullptr;
+void set_lapack(dgelsd64_t gelsd, dsyevd64_t syevd) {
+  g_dgelsd = gelsd;
+  g_dsyevd = syevd;
+}
+bool have_dgelsd() { return g_dgelsd != nullptr && g_dsyevd != nullptr; }
+
+// numpy/linalg/umath_linalg.cpp (lstsq gufunc): A copied column-major, b into a max(m, n) x 1
+// buffer, workspace sizes from an LWORK = -1 query, rcond = eps * max(m, n) (np.linalg.lstsq with
+// rcond=None); the solution is the first n entries of the b buffer.
+static void lstsq_dgelsd(int r, int c, const double* E, const double* g, double* w) {
+  typedef long long i64;
+  i64 m = r, n = c, nrhs = 1, lda = std::max<i64>(m, 1), ldb = std::max<i64>(std::max(m, n), 1), rank = 0,
+      info = 0, lwork = -1;
+  std::vector<double> A(size_t(m) * n), B(size_t(ldb), 0.0), S(size_t(std::min(m, n)));
+  for (i64 j = 0; j < n; ++j)
+    for (i64 i = 0; i < m; ++i) A[size_t(j * m + i)] = E[size_t(i) * c + j];
+  for (i64 i = 0; i < m; ++i) B[size_t(i)] = g[i];
+  const double rcond = 2.220446049250313e-16 * double(std::max(m, n));
+  double wq = 0.0;
+  i64 iwq = 0;
+  g_dgelsd(&m, &n, &nrhs, A.data(), &lda, B.data(), &ldb, S.data(), &rcond, &rank, &wq, &lwork, &iwq, &info);
+  if (info != 0) throw ValueErr("dgelsd workspace query failed (info " + std::to_string(info) + ")");
+  lwork = i64(wq);
+  std::vector<double> work(size_t(std::max<i64>(lwork, 1)));
+  std::vector<i64> iwork(size_t(std::max<i64>(iwq, 1)));
+  g_dgelsd(&m, &n, &nrhs, A.data(), &lda, B.data(), &ldb, S.data(), &rcond, &rank, work.data(), &lwork,
+           iwork.data(), &info);
+  if (info != 0) throw ValueErr("dgelsd: SVD did not converge (info " + std::to_string(info) + ")");
+  for (i64 j = 0; j < n; ++j) w[j] = B[size_t(j)];
+}
+
 // min-norm least squares E w = g (E: r x c, row-major) via one-sided Jacobi
 // SVD of E^T; singular values <= eps*max(r,c)*smax are dropped (gelsd rule).
 static void minnorm_lstsq(int r, int c, const double* E, const double* g, double* w) {
+  if (g_dgelsd) {
+    lstsq_dgelsd(r, c, E, g, w);
+    return;
+  }
   // A = E^T (c x r), columns a_k = row k of E
   std::vector<double> A(E, E + size_t(r) * c);  // A[k*c + i] = column k of E^T
   std::vector<double> V(size_t(r) * r, 0.0);

@@ -37,6 +37,18 @@ struct Rule1D {
   Csr B[2];  // deriv 0, 1: npts x nfun
 };
 
+// LAPACK dgelsd, ILP64 (all integers 64-bit), Fortran calling convention
+typedef void (*dgelsd64_t)(const long long* m, const long long* n, const long long* nrhs, double* a,
+                           const long long* lda, double* b, const long long* ldb, double* s, const double* rcond,
+                           long long* rank, double* work, const long long* lwork, long long* iwork, long long* info);
+// LAPACK dsyevd, ILP64, Fortran convention (+ the two hidden character-argument lengths)
+typedef void (*dsyevd64_t)(const char* jobz, const char* uplo, const long long* n, double* a, const long long* lda,
+                           double* w, double* work, const long long* lwork, long long* iwork,
+                           const long long* liwork, long long* info, unsigned long jobz_len, unsigned long uplo_len);
+// register (both) or clear (nullptr) the host LAPACK used for bit-exact numpy parity
+void set_lapack(dgelsd64_t gelsd, dsyevd64_t syevd);
+bool have_dgelsd();
+
 Csr collocation(const Knots& kv, const std::vector<double>& x, int deriv);
 void gauss_rule(const Knots& kv, int npts, std::vector<double>& x, std::vector<double>& w);
 std::vector<double> wq_points(const Knots& kv, int extra);

@@ -104,7 +104,6 @@ void Stiffness::init(const int* p, const int* nknots, const double* const* knots
   m1p = (dir[0].m + 3) / 4 * 4;
   set_slab(0, dir[2].n_el);
   compute_flops();
-  analyse_stencil();
 }
 
 // CostMeter count (kron.py:90-96, operators.py:191-203) restricted to the
@@ -148,7 +147,6 @@ void Stiffness::set_slab(int elo, int ehi) {
   y_hi = std::min(ehi + z.p - 1, z.n);
   q_lo = z.elem_q0[elo];
   q_hi = z.elem_q0[ehi];
-  fused_plan.reset();
   fused2_plan.reset();
   coeffs_ready = false;
 }
@@ -263,6 +261,11 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
   if (K9) std::copy(K9, K9 + 9, k);
   const int m1 = dir[0].m, m2 = dir[1].m, m3 = q_hi - q_lo;  // local quadrature planes
   const long long nql = (long long)m1 * m2 * m3;
+  // J_dev / Kfield_dev are full-domain (Nq, 3, 3) arrays (like the grids set_coeffs takes): a slab
+  // handle reads its own quadrature planes from q_lo on
+  const size_t qoff = (size_t)9 * q_lo * m1 * m2;
+  if (J_dev) J_dev += qoff;
+  if (Kfield_dev) Kfield_dev += qoff;
   int blocks = std::min<long long>((nql + 255) / 256, 148LL * 16);
   coeff_kernel<<<blocks, 256, 0, s>>>(kind, dir[0].pts_d.ptr, dir[1].pts_d.ptr, dir[2].pts_d.ptr + q_lo, m1, m2, m3, m1p,
                                       a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], K9 ? 1 : 0, k[0], k[1],
@@ -334,7 +337,6 @@ void Stiffness::set_on_the_fly(int kind, const double* A, const double* K9, cuda
   coeff.release();
   otf = true;
   coeffs_ready = true;
-  fused_plan.reset();
   fused2_plan.reset();
 }
 
@@ -587,7 +589,7 @@ long long Stiffness::mass_flops() const {
 void Stiffness::apply(const double* x, double* y, cudaStream_t s) {
   if (!coeffs_ready) throw ValueErr("coefficient grids not set");
   if (otf) {
-    if (path != 1 && path != 3 && fused2_apply(*this, x, y, s)) return;
+    if (path != 1 && fused2_apply(*this, x, y, s)) return;
     // the element-blocked kernel cannot take this rule (or a composed path was asked for): evaluate
     // the grids for this apply only, as the reference's on-the-fly mode does per grid
     bool nz[6];
@@ -604,15 +606,12 @@ void Stiffness::apply(const double* x, double* y, cudaStream_t s) {
     std::swap(keep.ptr, cx.ptr);
     std::swap(keep.n, cx.n);
     otf = true;
-    fused_plan.reset();
     fused2_plan.reset();
     return;
   }
   if (path == 1) { apply_generic(x, y, s); return; }
   apply_fused(x, y, s);
 }
-
-void Stiffness::analyse_stencil() { stencil.ok = false; }
 
 }  // namespace mfwq
 

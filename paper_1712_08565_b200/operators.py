@@ -188,20 +188,20 @@ class StiffnessOperator:
         return out
 
     def set_path(self, path: str):
-        """'auto' | 'generic' | 'fused' | 'fused_v1' kernel path (all on the GPU)."""
-        _lib.check(_lib.lib().mfwq_stiffness_set_path(self._h, {"auto": 0, "generic": 1, "fused": 2, "fused_v1": 3}[path]))
+        """'auto' | 'generic' | 'fused' kernel path (all on the GPU)."""
+        _lib.check(_lib.lib().mfwq_stiffness_set_path(self._h, {"auto": 0, "generic": 1, "fused": 2}[path]))
 
     def info(self):
-        tm, so, dev = C.c_int(), C.c_int(), C.c_double()
-        _lib.check(_lib.lib().mfwq_stiffness_info(self._h, C.byref(tm), C.byref(so), C.byref(dev)))
-        return {"term_mask": tm.value, "stencil_ok": bool(so.value), "stencil_dev": dev.value}
+        tm, ok, nt = C.c_int(), C.c_int(), C.c_int()
+        _lib.check(_lib.lib().mfwq_stiffness_info(self._h, C.byref(tm), C.byref(ok), C.byref(nt)))
+        return {"term_mask": tm.value, "fused_ok": bool(ok.value), "kernel_terms": nt.value}
 
     # -- apply (operators.py:185-204) -----------------------------------------
     def apply(self, v, meter: CostMeter | None = None, out=None):
         if _dev.is_pinned_host(v):
             return self._apply_pinned(v, meter, out)
         x, host = _dev.to_device(v, self._in_len)
-        y = out if out is not None else _dev.empty(self._out_len)
+        y = _dev.check_out(out, self._out_len) if out is not None else _dev.empty(self._out_len)
         _lib.check(_lib.lib().mfwq_stiffness_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
                                                    C.c_void_p(_dev.stream_ptr())))
         if meter is not None:
@@ -225,7 +225,9 @@ class StiffnessOperator:
             raise ValueError("out must be a contiguous float64 host tensor of the output length")
         x = v.reshape(-1)
         if x.dtype != torch.float64 or not x.is_contiguous():
-            x = x.to(torch.float64).contiguous().pin_memory()
+            # a converted temporary could be recycled by torch's pinned allocator while the raw copy
+            # that reads it is still queued: the caller owns (and keeps alive) the input buffer
+            raise ValueError("apply_pipelined takes a contiguous float64 pinned host tensor")
         cur = torch.cuda.current_stream()
         # native pipeline (mfwq_stiffness_apply_host): H2D / kernel / D2H on three streams, two device
         # staging pairs per operator; no per-call Python stream or event objects
@@ -368,7 +370,7 @@ class MassOperator:
 
     def apply(self, v, meter: CostMeter | None = None, out=None):
         x, host = _dev.to_device(v, self.n_dofs)
-        y = out if out is not None else _dev.empty(self.n_dofs)
+        y = _dev.check_out(out, self.n_dofs) if out is not None else _dev.empty(self.n_dofs)
         _lib.check(_lib.lib().mfwq_mass_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
                                               C.c_void_p(_dev.stream_ptr())))
         if meter is not None:

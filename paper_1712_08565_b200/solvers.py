@@ -96,7 +96,7 @@ class FDPreconditioner:
 
     def apply(self, r, meter: CostMeter | None = None, out=None):
         x, host = _dev.to_device(r, self.n_dofs)
-        z = out if out is not None else _dev.empty(self.n_dofs)
+        z = _dev.check_out(out, self.n_dofs) if out is not None else _dev.empty(self.n_dofs)
         _lib.check(_lib.lib().mfwq_fd_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(z.data_ptr()),
                                             C.c_void_p(_dev.stream_ptr())))
         if meter is not None:

@@ -27,6 +27,19 @@ def test_matvec_matches_reference(golden, path):
     assert meter.flops == int(g["flops"])
 
 
+def test_matvec_product_rule_matches_reference(golden):
+    """The drop-in path end to end: the package's OWN rule builder (build_tensor_rule, bit-identical
+    to the reference's weights via numpy's dgelsd) -> setup_stiffness -> apply, at every fixture
+    degree including p = 8 and 10, against the reference's matvec output."""
+    name, g = golden
+    kv = M.KnotVector(int(g["p"]), g["knots"])
+    space = M.TensorSpace((kv, kv, kv))
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), geom_of(g["geom"]))
+    x = np.random.default_rng(0).standard_normal(space.n_dofs)
+    y = A.apply(x)
+    assert relerr(y, g["y"]) <= MATVEC_TOL, (name, relerr(y, g["y"]))
+
+
 def test_fd_apply_matches_reference(golden):
     name, g = golden
     if "fd_y" not in g:

@@ -40,6 +40,59 @@ def test_slab_windows_sum_to_global(p, n_el, world, kind):
     assert relerr(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
 
 
+def _bent_map():
+    """A general (non-analytic-kind) map whose Jacobian varies with all three coordinates: the
+    operator evaluates it on the host and uploads full-domain (Nq, 3, 3) arrays (MFWQ_GEOM_JACOBIAN)."""
+    def _map(xi):
+        return np.stack([xi[:, 0] + 0.1 * xi[:, 1] * xi[:, 2], xi[:, 1] + 0.05 * xi[:, 0] ** 2,
+                         xi[:, 2] * (1.0 + 0.2 * xi[:, 0])], axis=1)
+
+    def _jac(xi):
+        J = np.zeros((len(xi), 3, 3))
+        J[:, 0, 0] = 1.0
+        J[:, 0, 1] = 0.1 * xi[:, 2]
+        J[:, 0, 2] = 0.1 * xi[:, 1]
+        J[:, 1, 0] = 0.1 * xi[:, 0]
+        J[:, 1, 1] = 1.0
+        J[:, 2, 0] = 0.2 * xi[:, 2]
+        J[:, 2, 2] = 1.0 + 0.2 * xi[:, 0]
+        return J
+
+    return M.GeometryMap(3, "bent", _map, _jac)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_windows_sum_to_global_jacobian_and_kfield(world):
+    """Slab handles read their own quadrature planes of the full-domain J and K-field arrays
+    (a rank with q_lo > 0 must not reuse the bottom slab's Jacobians)."""
+    p, n_el = 3, 12
+    space = M.tensor_space(p, n_el)
+    rule = M.build_tensor_rule(space)
+    geom = _bent_map()
+
+    def K(X):  # per-point SPD diffusion, varying along x3
+        k = np.zeros((len(X), 3, 3))
+        k[:, 0, 0] = 1.0 + X[:, 2] ** 2
+        k[:, 1, 1] = 2.0 + X[:, 0]
+        k[:, 2, 2] = 1.5 + 0.5 * np.sin(3 * X[:, 2])
+        k[:, 0, 2] = k[:, 2, 0] = 0.1 * X[:, 1]
+        return k
+
+    A = M.setup_stiffness(space, rule, geom, K=K)
+    n = A.n
+    plane = n[0] * n[1]
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(A.n_dofs)).cuda()
+    ref = A.apply(x)
+    part = SlabPartition(n_el, p, n[2], world).validate()
+    y = torch.zeros_like(ref)
+    for r in range(world):
+        op = M.StiffnessOperator(space, rule, geom, K=K, _slab=part.elements(r))
+        vlo, vhi = part.in_window(r)
+        ylo, yhi = part.out_window(r)
+        y[ylo * plane:yhi * plane] += op.apply(x[vlo * plane:vhi * plane])
+    assert relerr(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+
+
 def test_fd_dir_ops_compose_to_apply():
     space = M.tensor_space(3, 10)
     P = M.FDPreconditioner(space)
