@@ -104,46 +104,67 @@ struct Maps {
   CUtensorMap m[12];  // per coefficient grid: 16 x 16 x 4 boxes, then 16 x 16 x 2 boxes (zero fill past the grid edge)
 };
 
-template <int NT>
+// Term set KS: bit 3a+b set when the term (a,b) runs in this kernel (0x111 diagonal C, 0x11B the
+// stored quarter ring's diagonal + C01, 0x1FF general); the t-th term is the t-th set bit.
+__host__ __device__ constexpr int popc9(int ks) {
+  int n = 0;
+  for (int i = 0; i < 9; ++i) n += (ks >> i) & 1;
+  return n;
+}
+__host__ __device__ constexpr int nth_bit(int ks, int t) {
+  for (int i = 0; i < 9; ++i)
+    if ((ks >> i) & 1) {
+      if (t == 0) return i;
+      --t;
+    }
+  return 0;
+}
+template <int KS>
 struct Terms {
-  __host__ __device__ static constexpr int a(int t) { return NT == 3 ? t : (NT == 5 ? (t < 3 ? t : t - 3) : t / 3); }
-  __host__ __device__ static constexpr int b(int t) {
-    return NT == 3 ? t : (NT == 5 ? (t < 3 ? t : (t == 3 ? 1 : 0)) : t % 3);
+  static constexpr int N = popc9(KS);
+  // bit index of term t, tabulated once (a(t) / b(t) fold to constants in the unrolled loops)
+  static constexpr int I0 = nth_bit(KS, 0), I1 = nth_bit(KS, 1), I2 = nth_bit(KS, 2), I3 = nth_bit(KS, 3),
+                       I4 = nth_bit(KS, 4), I5 = nth_bit(KS, 5), I6 = nth_bit(KS, 6), I7 = nth_bit(KS, 7),
+                       I8 = nth_bit(KS, 8);
+  __host__ __device__ static constexpr int idx(int t) {
+    return t == 0 ? I0 : t == 1 ? I1 : t == 2 ? I2 : t == 3 ? I3 : t == 4 ? I4 : t == 5 ? I5 : t == 6 ? I6 : t == 7 ? I7 : I8;
   }
+  __host__ __device__ static constexpr int a(int t) { return idx(t) / 3; }
+  __host__ __device__ static constexpr int b(int t) { return idx(t) % 3; }
 };
 // symmetric grid index of (a,b): 00,01,02,11,12,22 -> 0..5 (non-recursive so it folds after unrolling)
 __host__ __device__ constexpr int gkey(int a, int b) {
   return (a < b ? a : b) == 0 ? (a < b ? b : a) : ((a < b ? a : b) == 1 ? 2 + (a < b ? b : a) : 5);
 }
 __host__ __device__ constexpr int wtype(int a, int b, int l) { return 2 * (a == l) + (b == l); }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr bool grid_used(int g) {
   bool u = false;
-  for (int t = 0; t < NT; ++t) u = u || gkey(Terms<NT>::a(t), Terms<NT>::b(t)) == g;
+  for (int t = 0; t < Terms<KS>::N; ++t) u = u || gkey(Terms<KS>::a(t), Terms<KS>::b(t)) == g;
   return u;
 }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr int n_grids() {
   int n = 0;
-  for (int g = 0; g < 6; ++g) n += grid_used<NT>(g) ? 1 : 0;
+  for (int g = 0; g < 6; ++g) n += grid_used<KS>(g) ? 1 : 0;
   return n;
 }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr int grid_slot(int g) {  // position of grid g among used grids
   int n = 0;
-  for (int h = 0; h < g; ++h) n += grid_used<NT>(h) ? 1 : 0;
+  for (int h = 0; h < g; ++h) n += grid_used<KS>(h) ? 1 : 0;
   return n;
 }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr bool ztype_used(int w) {
   bool u = false;
-  for (int t = 0; t < NT; ++t) u = u || wtype(Terms<NT>::a(t), Terms<NT>::b(t), 2) == w;
+  for (int t = 0; t < Terms<KS>::N; ++t) u = u || wtype(Terms<KS>::a(t), Terms<KS>::b(t), 2) == w;
   return u;
 }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr bool ytype_used(int w) {
   bool u = false;
-  for (int t = 0; t < NT; ++t) u = u || wtype(Terms<NT>::a(t), Terms<NT>::b(t), 1) == w;
+  for (int t = 0; t < Terms<KS>::N; ++t) u = u || wtype(Terms<KS>::a(t), Terms<KS>::b(t), 1) == w;
   return u;
 }
 
@@ -197,71 +218,64 @@ __device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map,
 // z-elements per step: 2, except the 5-term kernel at p = 3, where one element per step halves the
 // stage buffers so that two CTAs fit in shared memory (ring p = 3: 2.78 -> 2.53 ms at n_el = 256;
 // at p = 4 the same change spills and measured no faster, 2.89 vs 2.94 ms)
-__host__ __device__ constexpr int zs_for(int p, int nt) {
-#ifdef MFWQ_NT5_ZS2  // timing experiments only
-  return 2;
-#endif
-#ifdef MFWQ_NT5_ZS1P4  // timing experiments only
-  if (nt == 5 && p == 4) return 1;
-#endif
-#ifdef MFWQ_NT3_ZS1  // timing experiments only: 3-term kernel, one element per step, 3 CTAs/SM
-  if (nt == 3 && p <= MFWQ_NT3_ZS1) return 1;
-#endif
-  return (nt == 5 && p == 3) ? 1 : 2;
+__host__ __device__ constexpr int zs_for(int p, int ks) {
+  return (ks == 0x11B && p == 3) ? 1 : 2;
 }
-__host__ __device__ constexpr int occ_for(int p, int nt) {
-#ifdef MFWQ_OCC6
-  if (nt == 3 && p == MFWQ_OCCP) return MFWQ_OCC6;
-#endif
-#ifdef MFWQ_NT3_ZS1
-  if (nt == 3 && p <= MFWQ_NT3_ZS1) return 3;
-#endif
-  return ((nt == 3 && p <= 6) || (nt == 5 && (p <= 2 || zs_for(p, nt) == 1))) ? 2 : 1;
+__host__ __device__ constexpr int occ_for(int p, int ks) {
+  return ks == 0x111 ? (p <= 6 ? 2 : 1) : ks == 0x11B ? ((p <= 2 || zs_for(p, ks) == 1) ? 2 : 1) : 1;
 }
-template <int P, int NT>
+// gradient components the term set needs (b of its terms)
+template <int KS>
+__host__ __device__ constexpr bool bused(int b) {
+  bool u = false;
+  for (int t = 0; t < Terms<KS>::N; ++t) u = u || Terms<KS>::b(t) == b;
+  return u;
+}
+template <int P, int KS>
 struct Occ {
-  static constexpr int MINB = occ_for(P, NT);
+  static constexpr int MINB = occ_for(P, KS);
 };
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr int n_xtypes() {
   int n = 0;
   for (int w = 0; w < 4; ++w) {
     bool u = false;
-    for (int t = 0; t < NT; ++t) u = u || wtype(Terms<NT>::a(t), Terms<NT>::b(t), 0) == w;
+    for (int t = 0; t < Terms<KS>::N; ++t) u = u || wtype(Terms<KS>::a(t), Terms<KS>::b(t), 0) == w;
     n += u ? 1 : 0;
   }
   return n;
 }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr int xslot(int w) {  // compact index of x-type w among used x-types
   int n = 0;
   for (int v = 0; v < w; ++v) {
     bool u = false;
-    for (int t = 0; t < NT; ++t) u = u || wtype(Terms<NT>::a(t), Terms<NT>::b(t), 0) == v;
+    for (int t = 0; t < Terms<KS>::N; ++t) u = u || wtype(Terms<KS>::a(t), Terms<KS>::b(t), 0) == v;
     n += u ? 1 : 0;
   }
   return n;
 }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr int n_ytypes() {
   int n = 0;
-  for (int w = 0; w < 4; ++w) n += ytype_used<NT>(w) ? 1 : 0;
+  for (int w = 0; w < 4; ++w) n += ytype_used<KS>(w) ? 1 : 0;
   return n;
 }
-template <int NT>
+template <int KS>
 __host__ __device__ constexpr int yslot(int w) {
   int n = 0;
-  for (int v = 0; v < w; ++v) n += ytype_used<NT>(v) ? 1 : 0;
+  for (int v = 0; v < w; ++v) n += ytype_used<KS>(v) ? 1 : 0;
   return n;
 }
 
 // shared-memory plan (doubles), shared by kernel and host launch code
-template <int P, int NT, int ZS, bool OTF>
+template <int P, int KS, int ZS, bool OTF>
 struct Smem {
+  static constexpr int NT = Terms<KS>::N;
   static constexpr int NB = P + 1, NW = P + 2;
   static constexpr int NBP = (NB + 1) & ~1, NWP = (NW + 1) & ~1;  // 16-byte aligned sub-tables
   static constexpr int ZT = 2 * NBP + 4 * NWP;                     // z-table doubles per plane
-  static constexpr int G = n_grids<NT>(), NX = n_xtypes<NT>(), NY = n_ytypes<NT>();
+  static constexpr int G = n_grids<KS>(), NX = n_xtypes<KS>(), NY = n_ytypes<KS>();
   static constexpr int CST = OTF ? 0 : ZS * 2 * G * 256;            // the TMA coefficient stage
   static constexpr int DMAX = TQ / 2 + P + 1;                      // DoF window bound
   static constexpr int KB = (DMAX + 3) / 4, VR = 4 * KB;           // By k-steps, v-window rows read
@@ -278,10 +292,10 @@ struct Smem {
   }
 };
 
-template <int P, int NT, int ZS, bool OTF>
-__global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
-    k_fused(const __grid_constant__ Params prm, const __grid_constant__ Maps maps) {
-  using L = Smem<P, NT, ZS, OTF>;
+template <int P, int KS, int ZS, bool OTF>
+__device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) {
+  using L = Smem<P, KS, ZS, OTF>;
+  constexpr int NT = Terms<KS>::N;
   constexpr int NB = L::NB, NW = L::NW, NBP = L::NBP, NWP = L::NWP, ZT = L::ZT, G = L::G;
   constexpr int R = NB;                          // ring slots (B side): pushed right before use
   constexpr int A = NW;                          // accumulator slots (W side): retired per element
@@ -289,7 +303,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   constexpr int NTD = (DMAX + 7) / 8;            // 8-wide tiles over a window dimension
   constexpr int KB = L::KB, VR = L::VR;          // k-steps over window rows (By), rows of a v window
   static_assert(DMAX <= PV, "window exceeds tile pitch");
-  using T = Terms<NT>;
+  using T = Terms<KS>;
 
   const int QE = prm.qe;  // max quadrature planes per z-element
   extern __shared__ __align__(128) double sm[];
@@ -333,8 +347,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     copy16(sBy, yb, 2 * TQ * PKB);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      if (xslot<NT>(w + 1) > xslot<NT>(w)) copy16(sWxT + xslot<NT>(w) * TQ * PV, xb + w * TQ * PV, TQ * PV);
-      if (ytype_used<NT>(w)) copy16(sWy + yslot<NT>(w) * PV * PK, yb + 2 * TQ * PKB + w * PV * PK, PV * PK);
+      if (xslot<KS>(w + 1) > xslot<KS>(w)) copy16(sWxT + xslot<KS>(w) * TQ * PV, xb + w * TQ * PV, TQ * PV);
+      if (ytype_used<KS>(w)) copy16(sWy + yslot<KS>(w) * PV * PK, yb + 2 * TQ * PKB + w * PV * PK, PV * PK);
     }
     copy16(sBx, xb + 4 * TQ * PV, 2 * TQ * NB);
     cp_commit();
@@ -352,8 +366,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     if constexpr (OTF) {
 #pragma unroll
       for (int g = 0; g < 6; ++g)
-        if (grid_used<NT>(g) && tid < TQ)
-          sCx[grid_slot<NT>(g) * TQ + tid] = tid < tx.nq ? prm.cx[(size_t)g * prm.m[0] + tx.q0 + tid] : 0.0;
+        if (grid_used<KS>(g) && tid < TQ)
+          sCx[grid_slot<KS>(g) * TQ + tid] = tid < tx.nq ? prm.cx[(size_t)g * prm.m[0] + tx.q0 + tid] : 0.0;
     }
     cp_wait_all();
   }
@@ -421,7 +435,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       int g = 0;
 #pragma unroll
       for (int h = 0; h < 6; ++h)
-        if (grid_used<NT>(h) && grid_slot<NT>(h) == sl) g = h;
+        if (grid_used<KS>(h) && grid_slot<KS>(h) == sl) g = h;
       tma_load_3d(sC + sl * (2 * ZS) * 256, &maps.m[(ZS == 2 ? 0 : 6) + g], sInf->q0x, sInf->q0y, qa - prm.qzb, &mbar[0]);
     }
   };
@@ -441,11 +455,10 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     const double* b0 = sBx + ql1 * NB;
     const double* b1 = b0 + TQ * NB;
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      const double c0 = b0[k], c1 = b1[k], x0 = a0[k];
-      vx = fma(c1, x0, vx);
-      v0 = fma(c0, x0, v0);
-      vy = fma(c0, a1[k], vy);
+    for (int k = 0; k < NB; ++k) {  // only the gradient components the term set uses
+      if constexpr (bused<KS>(0)) vx = fma(b1[k], a0[k], vx);
+      if constexpr (bused<KS>(2)) v0 = fma(b0[k], a0[k], v0);
+      if constexpr (bused<KS>(1)) vy = fma(b0[k], a1[k], vy);
     }
 #pragma unroll
     for (int k = 0; k < R - 1; ++k) {
@@ -458,9 +471,13 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     h0[R - 1] = v0;
   };
   // B side, in-plane: DMMA y-contraction of nz planes of sV -> sA
+  // By types needed: 0 (By) for the x- and z-gradients, 1 (dBy) for the y-gradient
+  constexpr bool kA0 = bused<KS>(0) || bused<KS>(2), kA1 = bused<KS>(1);
+  constexpr int NBY = (kA0 ? 1 : 0) + (kA1 ? 1 : 0);
   auto bside_y = [&](int nz) {
-    for (int task = warp; task < ((MFWQ_ABLATE == 2 || (MFWQ_ABL_MASK & 1)) ? 0 : 2 * 2 * NTD); task += NWARP) {  // (b, mt, nt)
-      const int b = task / (2 * NTD), mt = (task / NTD) % 2, nt = task % NTD;
+    for (int task = warp; task < ((MFWQ_ABLATE == 2 || (MFWQ_ABL_MASK & 1)) ? 0 : NBY * 2 * NTD); task += NWARP) {  // (b, mt, nt)
+      const int bs = task / (2 * NTD), mt = (task / NTD) % 2, nt = task % NTD;
+      const int b = NBY == 2 ? bs : (kA0 ? 0 : 1);
       const double* ap = sBy + (b * TQ + mt * 8 + (lane >> 2)) * PKB + (lane & 3);
       double a[KB];
 #pragma unroll
@@ -512,8 +529,8 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          if (yslot<NT>(wtype(T::a(t), T::b(t), 1)) != ys) continue;  // warp-uniform
-          const int xs = xslot<NT>(wtype(T::a(t), T::b(t), 0));
+          if (yslot<KS>(wtype(T::a(t), T::b(t), 1)) != ys) continue;  // warp-uniform
+          const int xs = xslot<KS>(wtype(T::a(t), T::b(t), 0));
           const double* ap = sT + ((z * NT + t) * TQ + mt * 8 + (lane >> 2)) * PK + (lane & 3);
           const double* bp = sWxT + (xs * TQ + (lane & 3)) * PV + ((nt * 8 + (lane >> 2)) ^ swz(lane & 3));
           dmma(d0, d1, ap[0], bp[0]);
@@ -537,12 +554,12 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       int chain = 0;
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        if (!ytype_used<NT>(w)) continue;
+        if (!ytype_used<KS>(w)) continue;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const int kq = ks * 4 + (lane & 3);
-          const double a = sWy[(yslot<NT>(w) * PV + mt * 8 + (lane >> 2)) * PK + kq];
-          const double bb = sS[((z * L::NY + yslot<NT>(w)) * TQ + kq) * PV + ((nt * 8 + (lane >> 2)) ^ swz(lane & 3))];
+          const double a = sWy[(yslot<KS>(w) * PV + mt * 8 + (lane >> 2)) * PK + kq];
+          const double bb = sS[((z * L::NY + yslot<KS>(w)) * TQ + kq) * PV + ((nt * 8 + (lane >> 2)) ^ swz(lane & 3))];
           if (chain++ & 1) dmma(e0, e1, a, bb);
           else dmma(d0, d1, a, bb);
         }
@@ -574,13 +591,13 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     for (int k2 = 0; k2 < NBP / 2; ++k2) {
       const double2 c0 = zb0[k2], c1 = zb1[k2];
       const int k = 2 * k2;
-      gx = fma(c0.x, hx[ro + k], gx);
-      gy = fma(c0.x, hy[ro + k], gy);
-      gz = fma(c1.x, h0[ro + k], gz);
+      if constexpr (bused<KS>(0)) gx = fma(c0.x, hx[ro + k], gx);
+      if constexpr (bused<KS>(1)) gy = fma(c0.x, hy[ro + k], gy);
+      if constexpr (bused<KS>(2)) gz = fma(c1.x, h0[ro + k], gz);
       if (k + 1 < NB) {
-        gx = fma(c0.y, hx[ro + k + 1], gx);
-        gy = fma(c0.y, hy[ro + k + 1], gy);
-        gz = fma(c1.y, h0[ro + k + 1], gz);
+        if constexpr (bused<KS>(0)) gx = fma(c0.y, hx[ro + k + 1], gx);
+        if constexpr (bused<KS>(1)) gy = fma(c0.y, hy[ro + k + 1], gy);
+        if constexpr (bused<KS>(2)) gz = fma(c1.y, h0[ro + k + 1], gz);
       }
     }
     if (MFWQ_ABLATE == 3) return;
@@ -589,9 +606,9 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     double cg[6];
 #pragma unroll
     for (int g = 0; g < 6; ++g) {
-      if (!grid_used<NT>(g)) { cg[g] = 0.0; continue; }
-      if constexpr (OTF) cg[g] = active ? sCx[grid_slot<NT>(g) * TQ + ql1] : 0.0;
-      else if constexpr (kTMA) cg[g] = active ? cst[grid_slot<NT>(g) * (2 * ZS) * 256] : 0.0;
+      if (!grid_used<KS>(g)) { cg[g] = 0.0; continue; }
+      if constexpr (OTF) cg[g] = active ? sCx[grid_slot<KS>(g) * TQ + ql1] : 0.0;
+      else if constexpr (kTMA) cg[g] = active ? cst[grid_slot<KS>(g) * (2 * ZS) * 256] : 0.0;
       else cg[g] = active ? __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * prm.m[1] + sInf->q0y + ql2) * prm.m1p + sInf->q0x + ql1) : 0.0;
     }
     double tv[NT];
@@ -636,13 +653,13 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
         const double2 c0 = reinterpret_cast<const double2*>(zr + pl * zs)[k2];
         const double2 c1 = reinterpret_cast<const double2*>(zr + pl * zs + NBP)[k2];
         const int k = 2 * k2;
-        g[pl][0] = fma(c0.x, hx[k], g[pl][0]);
-        g[pl][1] = fma(c0.x, hy[k], g[pl][1]);
-        g[pl][2] = fma(c1.x, h0[k], g[pl][2]);
+        if constexpr (bused<KS>(0)) g[pl][0] = fma(c0.x, hx[k], g[pl][0]);
+        if constexpr (bused<KS>(1)) g[pl][1] = fma(c0.x, hy[k], g[pl][1]);
+        if constexpr (bused<KS>(2)) g[pl][2] = fma(c1.x, h0[k], g[pl][2]);
         if (k + 1 < NB) {
-          g[pl][0] = fma(c0.y, hx[k + 1], g[pl][0]);
-          g[pl][1] = fma(c0.y, hy[k + 1], g[pl][1]);
-          g[pl][2] = fma(c1.y, h0[k + 1], g[pl][2]);
+          if constexpr (bused<KS>(0)) g[pl][0] = fma(c0.y, hx[k + 1], g[pl][0]);
+          if constexpr (bused<KS>(1)) g[pl][1] = fma(c0.y, hy[k + 1], g[pl][1]);
+          if constexpr (bused<KS>(2)) g[pl][2] = fma(c1.y, h0[k + 1], g[pl][2]);
         }
       }
     double tv[2][NT];
@@ -651,9 +668,9 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
       double cg[6];
 #pragma unroll
       for (int gg = 0; gg < 6; ++gg) {
-        if (!grid_used<NT>(gg)) { cg[gg] = 0.0; continue; }
-        if constexpr (OTF) cg[gg] = active ? sCx[grid_slot<NT>(gg) * TQ + ql1] : 0.0;
-        else cg[gg] = active ? cst[pl * 256 + grid_slot<NT>(gg) * (2 * ZS) * 256] : 0.0;
+        if (!grid_used<KS>(gg)) { cg[gg] = 0.0; continue; }
+        if constexpr (OTF) cg[gg] = active ? sCx[grid_slot<KS>(gg) * TQ + ql1] : 0.0;
+        else cg[gg] = active ? cst[pl * 256 + grid_slot<KS>(gg) * (2 * ZS) * 256] : 0.0;
       }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
@@ -663,7 +680,7 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
     }
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      if (!ztype_used<NT>(w)) continue;
+      if (!ztype_used<KS>(w)) continue;
       const double* w0 = zr + 2 * NBP + w * NWP;
 #pragma unroll
       for (int k2 = 0; k2 < NWP / 2; ++k2) {
@@ -797,6 +814,13 @@ __global__ void __launch_bounds__(NTHR, Occ<P, NT>::MINB)
   PROF_DUMP
 }
 
+// one term set per launch (blockIdx.x: in-plane tile, blockIdx.y: z-chunk)
+template <int P, int KS, int ZS, bool OTF>
+__global__ void __launch_bounds__(NTHR, Occ<P, KS>::MINB)
+    k_fused(const __grid_constant__ Params prm, const __grid_constant__ Maps maps) {
+  fused_body<P, KS, ZS, OTF>(prm, maps);
+}
+
 }  // namespace f2
 
 // ---------------------------------------------------------------------------
@@ -901,8 +925,8 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
       // occupancy the kernel gets (2 or 1 CTAs per SM)
       const long long inplane = (long long)F->ntile[0] * F->ntile[1];
       const int mask = S.term_mask();
-      const int nt = (mask & ~0x111) == 0 ? 3 : ((mask & ~0x11B) == 0 ? 5 : 9);
-      const int occ = f2::occ_for(p, nt);
+      const int ks = (mask & ~0x111) == 0 ? 0x111 : ((mask & ~0x11B) == 0 ? 0x11B : 0x1FF);
+      const int occ = f2::occ_for(p, ks);
       int dev = 0, nsm = 148;
       if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const long long slots = (long long)occ * nsm;
@@ -1038,12 +1062,7 @@ void f2_zero_and_chain(double* y, long long n, cudaStream_t s) {
 void f2_zero_and_chain(double* y, long long n, cudaStream_t s);
 #endif
 
-template <int P, int NT, bool OTF>
-static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
-  constexpr int ZS = f2::zs_for(P, NT);
-  using namespace f2;
-  if constexpr (!OTF) encode_maps(S, F);
-  Params prm;
+static void fill_params(Stiffness& S, Fused2Plan& F, const double* x, double* y, f2::Params& prm) {
   for (int l = 0; l < 3; ++l) {
     prm.B[l] = F.B[l].ptr;
     prm.W[l] = F.W[l].ptr;
@@ -1078,13 +1097,18 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   prm.n3 = S.dir[2].n;
   prm.qe = F.qe;
   prm.cx = S.cx.ptr;
-  const size_t smem = Smem<P, NT, ZS, OTF>::bytes(F.qe, F.max_chunk);
-  auto kern = k_fused<P, NT, ZS, OTF>;
+}
+
+// zero w (releasing the fused kernel early), then the fused kernel with programmatic stream
+// serialisation: grid (in-plane tiles, z-chunks, term subsets)
+template <typename K>
+static void launch_chained(Stiffness& S, Fused2Plan& F, K kern, size_t smem, int nsub, const f2::Params& prm,
+                           double* y, cudaStream_t s) {
   MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   f2_zero_and_chain(y, (long long)S.out_elems(), s);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(F.ntile[0] * F.ntile[1], F.ntile[2]);
-  cfg.blockDim = dim3(NTHR);
+  cfg.gridDim = dim3(F.ntile[0] * F.ntile[1], F.ntile[2], nsub);
+  cfg.blockDim = dim3(f2::NTHR);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1097,21 +1121,31 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   MFWQ_CUDA(cudaGetLastError());
 }
 
+template <int P, int KS, bool OTF>
+static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
+  constexpr int ZS = f2::zs_for(P, KS);
+  using namespace f2;
+  if constexpr (!OTF) encode_maps(S, F);
+  Params prm;
+  fill_params(S, F, x, y, prm);
+  launch_chained(S, F, k_fused<P, KS, ZS, OTF>, Smem<P, KS, ZS, OTF>::bytes(F.qe, F.max_chunk), 1, prm, y, s);
+}
+
 template <int P, bool OTF>
 static void dispatch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
   const int mask = S.term_mask();
-  if ((mask & ~0x111) == 0) launch2<P, 3, OTF>(S, F, x, y, s);
-  else if ((mask & ~0x11B) == 0) launch2<P, 5, OTF>(S, F, x, y, s);
-  else launch2<P, 9, OTF>(S, F, x, y, s);
+  if ((mask & ~0x111) == 0) launch2<P, 0x111, OTF>(S, F, x, y, s);
+  else if ((mask & ~0x11B) == 0) launch2<P, 0x11B, OTF>(S, F, x, y, s);
+  else launch2<P, 0x1FF, OTF>(S, F, x, y, s);
 }
 
 template <bool OTF>
 static bool dispatch_p(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
-#ifdef MFWQ_ONLY_P  // static-analysis builds of one degree (tools/sass_stats.sh); never in the product
+#ifdef MFWQ_ONLY_P  // static-analysis / experiment builds of one degree (tools/sass_stats.sh); never in the product
   if (F.p != MFWQ_ONLY_P) return false;
   dispatch2<MFWQ_ONLY_P, OTF>(S, F, x, y, s);
   return true;
-#endif
+#else
   switch (F.p) {
     case 1: dispatch2<1, OTF>(S, F, x, y, s); break;
     case 2: dispatch2<2, OTF>(S, F, x, y, s); break;
@@ -1126,6 +1160,7 @@ static bool dispatch_p(Stiffness& S, Fused2Plan& F, const double* x, double* y, 
     default: return false;
   }
   return true;
+#endif
 }
 
 #ifndef MFWQ_F2_OTF_UNIT
