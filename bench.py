@@ -33,6 +33,18 @@ SWEEP = (2, 3, 4, 5, 6)
 N_EL = 128
 METRIC = "MF-WQ fp64 matvec DoF/s (cfg2 sweep p=2-6, n_el=128)"
 UNIT = "DoF/s"
+# the workload both arms run (identical dict in both JSON lines); arm-specific detail goes to "execution"
+CONFIG = {"workload": "cfg2 unit-cube MF-WQ matvec sweep: one matvec per degree p=2..6 per step, n_el=128",
+          "sweep": list(SWEEP), "n_el": N_EL, "geometry": "identity", "x": "N(0,1) seed 0"}
+ANCHORS = os.path.join(ROOT, "tests", "golden", "full_vectors.json")  # reference-run anchors (make_anchors.py)
+
+
+def anchors():
+    try:
+        with open(ANCHORS) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
 
 
 def parse():
@@ -241,9 +253,8 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "cfg2 unit-cube MF-WQ matvec, n_el=128, p=2..6 sweep",
-                       "sweep": list(SWEEP), "n_el": N_EL, "geometry": "identity",
-                       "parallelism": f"host: {nw} single-threaded processes"},
+            "config": dict(CONFIG),
+            "execution": {"parallelism": f"host: {nw} single-threaded processes"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": nw, "kind": "port",
                              "host_cores": cores,
                              "sample": f"{nw} worker processes (one per core, degree p = 2..6 round-robin), each "
@@ -357,6 +368,7 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = dofs_step * e2e_steps * world / (float(e2e_t) * 1e-3)
     pcie = pcie_probe(torch, hx, ops, stream)
+    dropin = dropin_e2e(torch, ops, dofs_step, e2e_steps)
 
     # on-the-fly coefficients (reference on_the_fly=True, operators.py:171-183): same sweep with C
     # evaluated in-kernel from C(xi1) instead of read from the N_q grids (secondary figure)
@@ -395,11 +407,14 @@ def run_ours(args, rank, world, local):
             "fp64_frac": fp64 / pk["fp64_tflops"], "fp64_src": pk["fp64_src"],
             "algorithmic_bytes": "8*(2N + G*Nq) per matvec, G = non-zero coefficient grids (3 on identity)"}
 
-    pcg = None
+    pcg = cfg4 = cfg1 = None
     if args.pcg and world == 1:
         pcg = run_pcg(M, torch, dev)
         pcg["on_the_fly_variant"] = {k: v for k, v in run_pcg(M, torch, dev, otf=True).items()
-                                     if k in ("iterations", "converged", "solve_s", "u_norm", "device_memory_used_gb")}
+                                     if k in ("iterations", "converged", "solve_s", "u_norm", "device_memory_used_gb",
+                                              "matvec", "anchor")}
+        cfg4 = run_cfg4(M, torch, dev)
+        cfg1 = run_cfg1(M, torch, dev)
     elif args.pcg:
         pcg = run_dist_pcg(M, torch, dev, rank, world)
 
@@ -414,21 +429,25 @@ def run_ours(args, rank, world, local):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "cfg2 unit-cube MF-WQ matvec, n_el=128, p=2..6 sweep per step",
-                           "sweep": list(SWEEP), "n_el": N_EL, "geometry": "identity",
-                           "x": "N(0,1) seed 0", "l2": "coefficient grids 0.4-0.9 GB per degree > 126 MB L2 (no flush)",
-                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                           "path": args.path},
+                "config": dict(CONFIG),
+                "execution": {"l2": "coefficient grids 0.4-0.9 GB per degree > 126 MB L2 (no flush)",
+                              "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                              "path": args.path},
                 "per_degree_us": {str(p): 1e3 * med[p] for p in SWEEP},
                 "per_degree_dofs": {str(p): ops[p]["N"] for p in SWEEP},
                 "roofline": roof,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "pcie": pcie,
-                        "h2d_bytes_per_step": 8 * dofs_step, "d2h_bytes_per_step": 8 * dofs_step},
+                        "h2d_bytes_per_step": 8 * dofs_step, "d2h_bytes_per_step": 8 * dofs_step,
+                        "api": "StiffnessOperator.apply_pipelined on pinned host tensors (H2D / kernel / D2H "
+                               "overlapped across calls)",
+                        "dropin": dropin},
                 "gpu_launches": int(launches),
                 "clocks": clk.summary(),
                 "on_the_fly": otf,
-                "pcg": pcg}
+                "pcg": pcg,
+                "cfg4": cfg4,
+                "cfg1": cfg1}
         print(json.dumps(line), flush=True)
 
 
@@ -501,8 +520,31 @@ def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1, otf=False):
         torch.cuda.synchronize()
         fts.append(e0.elapsed_time(e1) * 1e-3)
     fsec = sorted(fts)[len(fts) // 2]
-    fd_flops = sum(2 * 2 * n * n * space.n_dofs // n for n in space.n_per_dir) + space.n_dofs
+    # the matvec alone on x ~ N(0,1) seed 0, with its roofline (stored grids: 8 (2N + G Nq) bytes,
+    # G = non-zero grids; on the fly: 16 N bytes, so the fp64 roof is the binding one)
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(space.n_dofs)).to(dev)
+    y = torch.empty_like(x)
+    A.apply(x, out=y)
+    mts = []
+    for _ in range(9):
+        e0.record()
+        A.apply(x, out=y)
+        e1.record()
+        torch.cuda.synchronize()
+        mts.append(e0.elapsed_time(e1) * 1e-3)
+    msec = sorted(mts)[len(mts) // 2]
+    tm = A.info()["term_mask"]
+    grids = 0 if otf else len({(min(a, b), max(a, b)) for a in range(3) for b in range(3) if tm >> (3 * a + b) & 1})
+    mbytes = 8 * (2 * space.n_dofs + grids * A.n_points)
     pk = peaks()
+    mv = {"us": msec * 1e6, "dofs_per_s": space.n_dofs / msec, "grids_read": grids, "bytes": mbytes,
+          "kernel_terms": A.info()["kernel_terms"],
+          "roofline": {"bound": "hbm" if not otf else "fp64", "achieved_gbs": mbytes / msec / 1e9,
+                       "peak_gbs": pk["hbm_gbs"], "hbm_frac": mbytes / msec / 1e9 / pk["hbm_gbs"],
+                       "fp64_achieved_tflops": A.kernel_flops / msec / 1e12,
+                       "fp64_frac": A.kernel_flops / msec / 1e12 / pk["fp64_tflops"],
+                       "flops": "reference CostMeter count of the active terms (no on-the-fly coefficient charge)"}}
+    fd_flops = sum(2 * 2 * n * n * space.n_dofs // n for n in space.n_per_dir) + space.n_dofs
     fd = {"apply_s": fsec, "flops": fd_flops, "tflops": fd_flops / fsec / 1e12, "peak_tflops": pk["fp64_tflops"],
           "frac": fd_flops / fsec / 1e12 / pk["fp64_tflops"], "bound": "tensor (fp64 DMMA)", "peak_src": pk["fp64_src"]}
     free, total = torch.cuda.mem_get_info()
@@ -511,8 +553,24 @@ def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1, otf=False):
             "final_rel_residual": rep.residuals[-1], "solve_s": sec,
             "dof_iters_per_s": space.n_dofs * rep.iterations / sec,
             "setup_s": {"wq_rule": t1 - t0, "coeff_grids": t2 - t1, "fd": t3 - t2},
-            "fd_apply": fd,
-            "u_norm": float(torch.linalg.vector_norm(u))}
+            "fd_apply": fd, "matvec": mv,
+            "u_norm": float(torch.linalg.vector_norm(u)),
+            "_u": u}
+
+
+def anchor_check(r, key):
+    """Iterations and ||u|| against the reference's own run at this configuration (make_anchors.py)."""
+    a = anchors().get(key)
+    u = r.pop("_u")
+    if not a:
+        return None
+    return {"ref_iterations": a["iterations"], "iter_diff": r["iterations"] - a["iterations"],
+            "u_norm_rel_diff": abs(float(torch_norm(u)) - a["norm"]) / a["norm"]}
+
+
+def torch_norm(u):
+    import torch
+    return torch.linalg.vector_norm(u)
 
 
 def pcie_probe(torch, hx, ops, stream):
@@ -547,7 +605,77 @@ def run_pcg(M, torch, dev, otf=False):
     """cfg 3: quarter ring, p=4, n_el=256 (17.2 M DoFs), FD-PCG to 1e-8 on b ~ N(0,1) seed 1."""
     r = solve_case(M, torch, dev, 4, 256, otf=otf)
     r["config"] = "cfg3 quarter ring p=4 n_el=256"
+    r["anchor"] = anchor_check(r, "cfg3_u")
     return r
+
+
+CFG4 = ((2, 128), (4, 126), (6, 124), (8, 122), (10, 120))
+
+
+def run_cfg4(M, torch, dev):
+    """BASELINE configs[3]: k-method sweep on the quarter ring, N = 128^3 at every degree; per-phase
+    setup times (WQ rule, coefficient grids, FD eigendecomposition), FD-PCG to 1e-8, matvec roofline,
+    iterations / ||u|| against the reference's run."""
+    out = {}
+    for p, n_el in CFG4:
+        r = solve_case(M, torch, dev, p, n_el)
+        r["anchor"] = anchor_check(r, f"cfg4_p{p}_u")
+        out[str(p)] = {k: r[k] for k in ("N", "iterations", "converged", "solve_s", "setup_s", "matvec", "anchor")}
+        out[str(p)]["n_el"] = n_el
+        out[str(p)]["fd_apply_s"] = r["fd_apply"]["apply_s"]
+    return out
+
+
+def run_cfg1(M, torch, dev):
+    """BASELINE configs[0] on the GPU: p=3, n_el=16 unit cube; one matvec on x = default_rng(0) (median of
+    100, CUDA events) and FD-PCG to 1e-8 on the cube-sine load vector (host wall clock per solve)."""
+    space = M.tensor_space(3, 16)
+    geom = M.identity_map(3)
+    A = M.setup_stiffness(space, M.build_tensor_rule(space), geom)
+    P = M.FDPreconditioner(space)
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(space.n_dofs)).to(dev)
+    b = M.assemble_rhs(space, geom, M.cube_sine_case().f)
+    b = (b if torch.is_tensor(b) else torch.as_tensor(b)).to(dev)
+    y = torch.empty_like(x)
+    for _ in range(5):
+        A.apply(x, out=y)
+        u, rep = M.cg(A.apply, b, P.apply, tol=1e-8)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mts = []
+    for _ in range(100):
+        e0.record()
+        A.apply(x, out=y)
+        e1.record()
+        torch.cuda.synchronize()
+        mts.append(e0.elapsed_time(e1) * 1e3)
+    walls = []
+    for _ in range(50):
+        t0 = time.perf_counter()
+        u, rep = M.cg(A.apply, b, P.apply, tol=1e-8)
+        torch.cuda.synchronize()
+        walls.append((time.perf_counter() - t0) * 1e6)
+    return {"N": space.n_dofs, "matvec_us": statistics.median(mts), "pcg_wall_us": statistics.median(walls),
+            "iterations": rep.iterations, "u_norm": float(torch.linalg.vector_norm(u)),
+            "matvec_norm": float(torch.linalg.vector_norm(y))}
+
+
+def dropin_e2e(torch, ops, dofs_step, steps):
+    """The reference user's call: A.apply(numpy x) -> numpy y (pageable host memory, synchronous like
+    the reference's numpy semantics), over the cfg2 sweep; host wall clock."""
+    hx = {p: ops[p]["x"].cpu().numpy() for p in SWEEP}
+    for p in SWEEP:
+        ops[p]["A"].apply(hx[p])
+    torch.cuda.synchronize()
+    n = max(1, min(steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        for p in SWEEP:
+            yh = ops[p]["A"].apply(hx[p])
+    dt = time.perf_counter() - t0
+    assert isinstance(yh, np.ndarray)
+    return {"value": dofs_step * n / dt, "unit": UNIT, "api": "StiffnessOperator.apply(np.ndarray) -> np.ndarray",
+            "h2d_bytes_per_step": 8 * dofs_step, "d2h_bytes_per_step": 8 * dofs_step, "steps": n}
 
 
 def main():

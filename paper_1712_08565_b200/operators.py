@@ -112,6 +112,7 @@ class StiffnessOperator:
         self.apply_flops = fl.value + fly
         _lib.check(L.mfwq_stiffness_flops_active(self._h, C.byref(fl)))
         self.apply_flops_active = fl.value + fly  # terms with a non-zero coefficient (what runs)
+        self.kernel_flops = fl.value  # the same without the reference's nominal coefficient charges
         self.setup_flops = 0 if self.on_the_fly else COEFF_EVAL_FLOPS * self.n_points * 6
 
     def _set_on_the_fly(self, geom, K):
