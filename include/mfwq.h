@@ -20,6 +20,7 @@
  *   mfwq_fd_create         FDPreconditioner.__init__                   solvers.py:72-101
  *   mfwq_fd_apply          FDPreconditioner.apply                      solvers.py:107-115
  *   mfwq_pcg_solve         cg (device-resident loop)                   solvers.py:137-173
+ *   mfwq_pcg_solve_comm    cg over xi3 slabs (multi-GPU, NCCL)          solvers.py:137-173, 107-115
  *   mfwq_bicg_*, mfwq_dot2 bicgstab vector updates                     solvers.py:176-249
  *   mfwq_stiffness_set_on_the_fly  on_the_fly=True coefficient mode    operators.py:171-183, 207-220
  *   mfwq_mass_*            MassOperator / setup_mass                   operators.py:46-61, 87-132
@@ -204,6 +205,29 @@ typedef struct {
 /* P may be NULL (identity).  b_dev, x_dev: device vectors of length N. */
 int mfwq_pcg_solve(mfwq_stiffness_t A, mfwq_fd_t P, const double* b_dev, double* x_dev, double tol, int maxit,
                    double* residuals, mfwq_krylov_report* report, void* stream);
+
+/* ---------------- slab-distributed PCG: the `comm` variant ----------------------
+   The tensor grid is cut along xi3: rank r owns z-elements [E_r, E_r+1), E_r = r n_el / world,
+   and the interior DoF planes [E_r - 1, E_r+1 - 1) (rank 0 from 0, the last rank up to n3); its
+   vectors are that contiguous slice of the flat vector.  A communicator drives `nlocal` ranks from
+   this process: NCCL (one rank per process / GPU over NVLink) or the in-process transport (every
+   rank of the partition from one process on one device, one cudaMemcpyAsync per message; the
+   single-GPU emulation of the multi-GPU path with the same solver, kernels and messages). */
+typedef struct mfwq_comm_s* mfwq_comm_t;
+/* nccl_lib: path of the NCCL shared library to use (torch's bundled libnccl.so.2) */
+int mfwq_nccl_unique_id(const char* nccl_lib, unsigned char* id128);
+int mfwq_comm_create_nccl(const char* nccl_lib, const unsigned char* id128, int world, int rank, mfwq_comm_t* out);
+int mfwq_comm_create_local(int world, mfwq_comm_t* out);
+int mfwq_comm_info(mfwq_comm_t c, int* world, int* nlocal, int* first_rank);
+void mfwq_comm_destroy(mfwq_comm_t c);
+/* cg (solvers.py:137-173) over the slabs, device resident: slabs[l] is local rank (first_rank + l)'s
+   slab operator (mfwq_stiffness_set_slab with that rank's elements), P the FD preconditioner of the
+   whole space (required), b[l] / x[l] its owned slices (device).  Halo exchanges for the matvec,
+   all-to-all for the FD direction 3, allreduced scalars for the dots; one host read per iteration.
+   The report and residual history are the global ones (identical on every rank). */
+int mfwq_pcg_solve_comm(mfwq_comm_t comm, const mfwq_stiffness_t* slabs, mfwq_fd_t P, const double* const* b,
+                        double* const* x, double tol, int maxit, double* residuals, mfwq_krylov_report* report,
+                        void* stream);
 
 /* dense Kronecker apply y (+)= (A_d x ... x A_1) x on the device, direction d
    first (kron.py:70-100); A_l host row-major (rows[l] x cols[l]), d <= 3 */

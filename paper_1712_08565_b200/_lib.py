@@ -71,6 +71,14 @@ _SIGS = {
     "mfwq_fd_destroy": (None, [C.c_void_p]),
     "mfwq_pcg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
                                  dp, C.POINTER(KrylovReportC), C.c_void_p]),
+    "mfwq_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_char_p]),
+    "mfwq_comm_create_nccl": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "mfwq_comm_create_local": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "mfwq_comm_info": (C.c_int, [C.c_void_p, ip, ip, ip]),
+    "mfwq_comm_destroy": (None, [C.c_void_p]),
+    "mfwq_pcg_solve_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p, C.POINTER(C.c_void_p),
+                                      C.POINTER(C.c_void_p), C.c_double, C.c_int, dp, C.POINTER(KrylovReportC),
+                                      C.c_void_p]),
     "mfwq_dot": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, dp, C.c_void_p]),
     "mfwq_dot2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, dp, C.c_void_p]),
     "mfwq_axpy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, C.c_double, C.c_void_p]),

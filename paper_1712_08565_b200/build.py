@@ -17,11 +17,27 @@ BUILD = os.path.join(ROOT, "build", os.environ.get("MFWQ_BUILD_TAG", "mfwq"))
 LIB = os.environ.get("MFWQ_BUILD_LIB") or os.path.join(PKG, "libmfwq.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_include():
+    """nccl.h of the NCCL torch bundles (types only: libmfwq.so dlopens that library at run time)."""
+    try:
+        import nvidia.nccl as nc
+        base = list(nc.__path__)[0]
+    except ImportError:
+        base = ""
+    inc = os.path.join(base, "include")
+    if not os.path.exists(os.path.join(inc, "nccl.h")):
+        raise RuntimeError("nccl.h of torch's bundled NCCL (nvidia.nccl) not found")
+    return inc
+
+
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC] + os.environ.get("MFWQ_NVCC_EXTRA", "").split()
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()] + \
+    os.environ.get("MFWQ_NVCC_EXTRA", "").split()
 SOURCES = ["rule1d.cpp", "stiffness.cu", "fused2.cu", "fused2_otf.cu", "fd.cu", "modal_gemm.cu", "pcg.cu",
-           "bicgstab.cu", "quadrature.cu", "capi.cu"]
-LIBS = ["-lcusolver", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64"]
+           "bicgstab.cu", "quadrature.cu", "dist.cu", "capi.cu"]
+LIBS = ["-lcusolver", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64"]
 
 
 def _deps_mtime():

@@ -362,6 +362,58 @@ int mfwq_pcg_solve(mfwq_stiffness_t A, mfwq_fd_t P, const double* b, double* x, 
   });
 }
 
+struct mfwq_comm_s {
+  Transport* t = nullptr;
+  ~mfwq_comm_s() { transport_destroy(t); }
+};
+
+int mfwq_nccl_unique_id(const char* nccl_lib, unsigned char* id128) {
+  return guard([&] { nccl_unique_id(nccl_lib, id128); });
+}
+
+int mfwq_comm_create_nccl(const char* nccl_lib, const unsigned char* id128, int world, int rank, mfwq_comm_t* out) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) throw ValueErr("rank out of range");
+    auto* c = new mfwq_comm_s();
+    c->t = transport_nccl(nccl_lib, id128, world, rank);
+    *out = c;
+  });
+}
+
+int mfwq_comm_create_local(int world, mfwq_comm_t* out) {
+  return guard([&] {
+    auto* c = new mfwq_comm_s();
+    c->t = transport_local(world);
+    *out = c;
+  });
+}
+
+int mfwq_comm_info(mfwq_comm_t c, int* world, int* nlocal, int* first_rank) {
+  return guard([&] { transport_info(c->t, world, nlocal, first_rank); });
+}
+
+void mfwq_comm_destroy(mfwq_comm_t c) { delete c; }
+
+int mfwq_pcg_solve_comm(mfwq_comm_t comm, const mfwq_stiffness_t* slabs, mfwq_fd_t P, const double* const* b,
+                        double* const* x, double tol, int maxit, double* residuals, mfwq_krylov_report* rep,
+                        void* stream) {
+  return guard([&] {
+    int world, nl, first;
+    transport_info(comm->t, &world, &nl, &first);
+    std::vector<Stiffness*> ops(nl);
+    for (int l = 0; l < nl; ++l) ops[l] = &slabs[l]->op;
+    std::vector<double> hist;
+    KrylovOut o;
+    dist_pcg_solve(*comm->t, ops.data(), P ? &P->fd : nullptr, b, x, tol, maxit, hist, o, (cudaStream_t)stream);
+    rep->iterations = o.iterations;
+    rep->converged = o.converged;
+    rep->matvecs = o.matvecs;
+    rep->precond_applies = o.precs;
+    rep->n_residuals = int(hist.size());
+    std::memcpy(residuals, hist.data(), hist.size() * sizeof(double));
+  });
+}
+
 int mfwq_kron_apply(int d, const int* rows, const int* cols, const double* const* A, const double* x, double* y,
                     int accumulate, void* stream) {
   return guard([&] { kron_apply_dense(d, rows, cols, A, x, y, accumulate, (cudaStream_t)stream); });

@@ -46,6 +46,7 @@ class Stiffness {
   size_t out_elems() const { return size_t(y_hi - y_lo) * dir[0].n * dir[1].n; }
 
   DevBuf<double> pcg_ws;  // PCG work vectors (r, z, p, Ap) + reduction partials, reused across solves
+  DevBuf<double> dist_ws;  // slab-distributed PCG workspace of this rank (dist.cu)
 
   // on-the-fly coefficients (operators.py:171-183, 207-220): for the analytic maps C depends on
   // xi1 at most, so the kernel reads C(xi1) from a [6][m1] table instead of 6 N_q grids
@@ -123,6 +124,24 @@ void kron_apply_dense(int d, const int* rows, const int* cols, const double* con
 
 // vector kernels
 double dev_dot(const double* a, const double* b, long long N, cudaStream_t s);
+// PCG building blocks (pcg.cu): deterministic two-level dot into *out; x += a p, r -= a Ap with
+// a = *rz / *pAp and ||r||^2 into *rr; p = z + (*rz_new / *rz) p then *rz = *rz_new.
+// Vectors 16-byte aligned; `partial` holds vec_partials() doubles.
+void vec_dot_to(const double* a, const double* b, long long N, double* partial, double* out, cudaStream_t s);
+void vec_update_xr(double* x, double* r, const double* p, const double* Ap, long long N, const double* rz,
+                   const double* pAp, double* partial, double* rr, cudaStream_t s);
+void vec_update_p(double* p, const double* z, long long N, const double* rz_new, double* rz, cudaStream_t s);
+int vec_partials();
+
+// slab-distributed PCG (dist.cu): transports and the comm variant of pcg_solve
+struct Transport;
+Transport* transport_local(int world);
+Transport* transport_nccl(const char* lib, const unsigned char* id128, int world, int rank);
+void transport_destroy(Transport* t);
+void transport_info(const Transport* t, int* world, int* nlocal, int* first);
+void nccl_unique_id(const char* lib, unsigned char* id128);
+void dist_pcg_solve(Transport& T, Stiffness* const* slabs, FastDiag* P, const double* const* b, double* const* x,
+                    double tol, int maxit, std::vector<double>& hist, KrylovOut& out, cudaStream_t s);
 
 // BiCGStab fused vector updates (bicgstab.cu; solvers.py:176-249); reductions return to the host
 void bicg_p(double* p, const double* r, const double* v, long long N, double beta, double omega, cudaStream_t s);

@@ -116,6 +116,21 @@ static void dot_to(const double* a, const double* b, long long N, double* partia
   finish_sum<<<1, RB, 0, s>>>(partial, RGRID, out); note_launch();
 }
 
+// building blocks shared with the slab-distributed solver (dist.cu)
+void vec_dot_to(const double* a, const double* b, long long N, double* partial, double* out, cudaStream_t s) {
+  dot_to(a, b, N, partial, out, s);
+}
+void vec_update_xr(double* x, double* r, const double* p, const double* Ap, long long N, const double* rz,
+                   const double* pAp, double* partial, double* rr, cudaStream_t s) {
+  update_xr<<<RGRID, RB, 0, s>>>(x, r, p, Ap, N, rz, pAp, partial); note_launch();
+  finish_sum<<<1, RB, 0, s>>>(partial, RGRID, rr); note_launch();
+}
+void vec_update_p(double* p, const double* z, long long N, const double* rz_new, double* rz, cudaStream_t s) {
+  update_p<<<RGRID, RB, 0, s>>>(p, z, N, rz_new, rz); note_launch();
+  copy_scalar<<<1, 1, 0, s>>>(rz_new, rz); note_launch();
+}
+int vec_partials() { return RGRID; }
+
 double dev_dot(const double* a, const double* b, long long N, cudaStream_t s) {
   DevBuf<double> part(RGRID), out(1);
   dot_to(a, b, N, part.ptr, out.ptr, s);

@@ -269,6 +269,111 @@ def cuda_fd_dir_op(fd):
     return op
 
 
+# ---------------------------------------------------------------------------
+# native comm-aware solver (libmfwq.so mfwq_pcg_solve_comm): halo exchanges, FD all-to-all and
+# allreduced PCG scalars inside the library; one host read per iteration
+# ---------------------------------------------------------------------------
+def nccl_library():
+    """Path of the NCCL torch bundles (the one torch.distributed itself loaded)."""
+    import glob
+    import os
+    try:
+        import nvidia.nccl as nc
+        for base in nc.__path__:
+            hits = sorted(glob.glob(os.path.join(base, "lib", "libnccl.so*")))
+            if hits:
+                return hits[0]
+    except ImportError:
+        pass
+    raise RuntimeError("torch's bundled NCCL (nvidia.nccl) not found")
+
+
+class Communicator:
+    """Transport of the native slab solver: ``Communicator.local(P)`` drives all P ranks of the
+    partition from this process on the current device (single-GPU emulation of the multi-GPU path:
+    same solver, slab kernels and messages, one cudaMemcpyAsync per message), ``Communicator.nccl()``
+    is one rank per process / GPU over NCCL (NVLink), set up from a torch.distributed group."""
+
+    def __init__(self, handle):
+        from . import _lib
+        self._h = handle
+        w, nl, f = C.c_int(), C.c_int(), C.c_int()
+        _lib.check(_lib.lib().mfwq_comm_info(handle, C.byref(w), C.byref(nl), C.byref(f)))
+        self.world, self.nlocal, self.first = w.value, nl.value, f.value
+
+    @classmethod
+    def local(cls, world):
+        from . import _lib
+        h = C.c_void_p()
+        _lib.check(_lib.lib().mfwq_comm_create_local(int(world), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def nccl(cls, group=None):
+        from . import _lib
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        lib = nccl_library().encode()
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(_lib.lib().mfwq_nccl_unique_id(lib, uid))
+        obj = [bytes(uid.raw) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = C.create_string_buffer(obj[0], 128)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().mfwq_comm_create_nccl(lib, uid, world, rank, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None:
+            from . import _lib
+            if _lib._lib is not None:
+                _lib._lib.mfwq_comm_destroy(h)
+            self._h = None
+
+
+class SlabSolver:
+    """Slab-distributed FD-PCG (solvers.py:137-173) with the ranks this process drives.
+
+    ``cg(b_slices, tol, maxit)`` takes each local rank's owned slice of b (device tensors, planes
+    SlabPartition.owned(rank)) and returns (x slices, KrylovReport); the report is the global one."""
+
+    def __init__(self, space, rule, geom, comm: Communicator, K=None, on_the_fly=False):
+        from .operators import StiffnessOperator
+        from .solvers import FDPreconditioner
+        kv = space.knotvectors[2]
+        self.n = [k.n_funcs - 2 for k in space.knotvectors]
+        self.plane = self.n[0] * self.n[1]
+        self.part = SlabPartition(len(np.unique(kv.knots)) - 1, kv.degree, self.n[2], comm.world).validate()
+        self.comm = comm
+        self.ranks = list(range(comm.first, comm.first + comm.nlocal))
+        self.ops = [StiffnessOperator(space, rule, geom, K=K, on_the_fly=on_the_fly, _slab=self.part.elements(r))
+                    for r in self.ranks]
+        self.P = FDPreconditioner(space)
+
+    def owned_slices(self, full):
+        """The local ranks' owned slices of a full-length vector (views)."""
+        return [full[slice(*(v * self.plane for v in self.part.owned(r)))] for r in self.ranks]
+
+    def cg(self, b_slices, tol=1e-8, maxit=1000):
+        from . import _dev, _lib
+        from .solvers import KrylovReport
+        bs = [_dev.to_device(b, (self.part.owned(r)[1] - self.part.owned(r)[0]) * self.plane)[0]
+              for b, r in zip(b_slices, self.ranks)]
+        xs = [torch.empty_like(b) for b in bs]
+        n = len(bs)
+        ops = (C.c_void_p * n)(*[op._h for op in self.ops])
+        bp = (C.c_void_p * n)(*[b.data_ptr() for b in bs])
+        xp = (C.c_void_p * n)(*[x.data_ptr() for x in xs])
+        hist = np.zeros(maxit + 1)
+        rep = _lib.KrylovReportC()
+        _lib.check(_lib.lib().mfwq_pcg_solve_comm(self.comm._h, ops, self.P._h, bp, xp, float(tol), int(maxit),
+                                                  _lib.dptr(hist), C.byref(rep), C.c_void_p(_dev.stream_ptr())))
+        report = KrylovReport(rep.iterations, hist[:rep.n_residuals].tolist(), bool(rep.converged), rep.matvecs,
+                              rep.precond_applies)
+        return xs, report
+
+
 def setup_distributed(space, rule, geom, K=None, group=None):
     """(DistStiffness, DistFD, partition) for this rank, on its CUDA device."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
