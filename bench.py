@@ -9,10 +9,16 @@ explicit flush is needed between iterations.
 
 Extra keys: per-degree times, roofline of the matvec kernel (HBM bound per
 BASELINE; fp64 fraction alongside), e2e through the public API with pinned
-host buffers, the CPU baseline (oracle port on the host cores), and an
-optional cfg-3 FD-PCG time-to-solution (--pcg).
+host buffers (and through the drop-in numpy call), the CPU baseline (oracle
+port on the host cores), the cfg-3 matvec / FD-PCG, the cfg-4 per-phase
+k-sweep and cfg 1 (--pcg), and the cfg-5 FD-PCG on one GPU (--slab).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--pcg 0|1]
+With N > 1 (torchrun, or --gpus N, which spawns the ranks itself) the headline
+is the cfg-5 FD-PCG split into N xi3 slabs, one rank per GPU (strong scaling,
+native comm-aware solver over NCCL); the N = 1 line carries the same solve on
+one GPU under "slab_pcg" as its baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--pcg 0|1] [--slab 0|1]
 """
 
 import argparse
@@ -56,6 +62,7 @@ def parse():
     ap.add_argument("--pcg", type=int, default=1)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--path", default="auto", choices=["auto", "generic", "fused"])
+    ap.add_argument("--slab", type=int, default=1, help="cfg5 slab PCG (1-GPU baseline / N-GPU headline)")
     return ap.parse_args()
 
 
@@ -213,6 +220,54 @@ def _ref_workers():
         by_mem = cores
     cap = int(os.environ.get("MFWQ_REF_WORKERS", "0")) or cores
     return max(1, min(cores, by_mem, cap)), cores
+
+
+def run_reference_slab(args, rank, world):
+    """Reference arm of the N > 1 headline (cfg5 slab PCG): the oracle port's PCG iteration (one MF-WQ
+    matvec, one FD apply, the vector updates; solvers.py:154-172) on a bounded sample of the cfg5
+    problem -- the quarter ring at p = 6 with the full 512 x 512 element cross-section and a z-extent
+    of SLAB_SAMPLE_EL elements -- timed on rank 0's host cores; value = sample DoFs x iterations / s."""
+    if rank != 0:
+        return
+    from oracle import mfwq_oracle as O
+    p, n_el = CFG5
+    ez = int(os.environ.get("MFWQ_SLAB_SAMPLE_EL", "4"))
+    nxy = int(os.environ.get("MFWQ_SLAB_SAMPLE_NXY", str(n_el)))  # tests shrink the cross-section
+    kxy, kz = O.uniform_knots(p, nxy), O.uniform_knots(p, ez)
+    rules = [O.rule_1d(kxy), O.rule_1d(kxy), O.rule_1d(kz)]
+    A = O.Stiffness(rules, O.stiffness_coeffs(rules, O.jac_ring))
+    P = O.FD([kxy, kxy, kz])
+    r = np.random.default_rng(1).standard_normal(A.N)
+    pv = r.copy()
+    x = np.zeros(A.N)
+
+    def it():
+        Ap = A.apply(pv)
+        alpha = float(r @ r) / float(pv @ Ap)
+        x.__iadd__(alpha * pv)
+        rn = r - alpha * Ap
+        z = P.apply(rn)
+        return float(rn @ z)
+
+    for _ in range(max(1, min(args.warmup, 1))):
+        it()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        it()
+    dt = (time.perf_counter() - t0) / args.steps
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    val = A.N / dt
+    line = {"metric": SLAB_METRIC, "value": val, "unit": "DoF-iterations/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"cfg5 quarter ring p={p} n_el={n_el}, xi3 slabs x{world}",
+                       "parallelism": f"xi3 slabs x{world} (NCCL)"},
+            "cpu_baseline": {"value": val, "unit": "DoF-iterations/s", "cores": cores, "kind": "port",
+                             "sample": f"one oracle PCG iteration (MF-WQ matvec + FD apply + updates) per step on a "
+                                       f"{nxy} x {nxy} x {ez}-element z-slab of the cfg5 quarter ring (p={p}), "
+                                       f"{A.N} DoFs; scipy CSR single-threaded, FD dgemm on the host BLAS threads"},
+            "e2e": {"value": val, "unit": "DoF-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 def run_reference(args, rank, world):
@@ -415,8 +470,9 @@ def run_ours(args, rank, world, local):
                                               "matvec", "anchor")}
         cfg4 = run_cfg4(M, torch, dev)
         cfg1 = run_cfg1(M, torch, dev)
-    elif args.pcg:
-        pcg = run_dist_pcg(M, torch, dev, rank, world)
+    slab = None
+    if args.slab:  # cfg 5 strong scaling: the 1-GPU baseline here, the N-GPU headline in run_slab_headline
+        slab = run_slab_pcg(M, torch, dev, rank, world)
 
     if rank == 0:
         cpu = None
@@ -447,41 +503,69 @@ def run_ours(args, rank, world, local):
                 "on_the_fly": otf,
                 "pcg": pcg,
                 "cfg4": cfg4,
-                "cfg1": cfg1}
+                "cfg1": cfg1,
+                "slab_pcg": slab}
         print(json.dumps(line), flush=True)
 
 
-def run_dist_pcg(M, torch, dev, rank, world):
-    """cfg 3 on `world` GPUs: xi_3 slabs, halo exchange, all-to-all FD, allreduce dots (NCCL)."""
-    import torch.distributed as dist
-    from paper_1712_08565_b200.dist import dist_cg, setup_distributed
+SLAB_METRIC = "MF-WQ cfg5 slab FD-PCG DoF-iterations/s (quarter ring p=6, n_el=512, xi3 slabs, to 1e-8)"
+CFG5 = (6, 512)
 
-    p, n_el = 4, 256
+
+def run_slab_pcg(M, torch, dev, rank, world, steps=1, warmup=1):
+    """BASELINE configs[4]: the quarter ring at p=6, n_el=512 (137 M DoFs), FD-PCG to 1e-8 on
+    b = default_rng(1), split into `world` xi3 slabs, one rank per GPU: the native comm-aware solver
+    (mfwq_pcg_solve_comm; halo exchanges, FD all-to-all and allreduced scalars over NCCL).  world = 1
+    is the single-GPU device PCG (the strong-scaling baseline).  Time = max over ranks (CUDA events)."""
+    import torch.distributed as dist
+    p, n_el = CFG5
+    b_full = np.random.default_rng(1).standard_normal(M.tensor_space(p, n_el).n_dofs)
+    t0 = time.perf_counter()
     space = M.tensor_space(p, n_el)
     rule = M.build_tensor_rule(space)
-    A, P, part = setup_distributed(space, rule, M.quarter_ring_map())
-    lo, hi = part.owned(rank)
-    plane = A.plane
-    b_full = np.random.default_rng(1).standard_normal(space.n_dofs)
-    b = torch.from_numpy(b_full[lo * plane:hi * plane].copy()).to(dev)
-    dist_cg(A.apply, b, P.apply, tol=1e-8, maxit=2)  # warm-up
+    geom = M.quarter_ring_map()
+    t1 = time.perf_counter()
+    if world > 1:
+        from paper_1712_08565_b200.dist import Communicator, SlabSolver
+        S = SlabSolver(space, rule, geom, Communicator.nccl())
+        b = [torch.from_numpy(v.copy()).to(dev) for v in S.owned_slices(b_full)]
+        solve = lambda: S.cg(b, tol=1e-8)  # noqa: E731
+    else:
+        A = M.setup_stiffness(space, rule, geom)
+        P = M.FDPreconditioner(space)
+        b1 = torch.from_numpy(b_full).to(dev)
+        solve = lambda: M.cg(A.apply, b1, P.apply, tol=1e-8)  # noqa: E731
     torch.cuda.synchronize()
-    dist.barrier()
+    setup_s = time.perf_counter() - t1
+    for _ in range(warmup):
+        solve()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    u, rep = dist_cg(A.apply, b, P.apply, tol=1e-8)
+    for _ in range(steps):
+        u, rep = solve()
     e1.record()
     torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        u = u[0]
     nrm = torch.stack([(u * u).sum()])
-    dist.all_reduce(nrm)
+    if world > 1:
+        dist.all_reduce(nrm)
     secs = float(t)
-    return {"config": f"cfg3 quarter ring p=4 n_el=256, xi3 slabs x{world}", "N": space.n_dofs,
-            "iterations": rep.iterations, "converged": rep.converged, "final_rel_residual": rep.residuals[-1],
-            "solve_s": secs, "dof_iters_per_s": space.n_dofs * rep.iterations / secs,
-            "u_norm": float(nrm[0]) ** 0.5}
+    free, total = torch.cuda.mem_get_info()
+    return {"metric": SLAB_METRIC, "value": space.n_dofs * rep.iterations / secs, "unit": "DoF-iterations/s",
+            "scaling": "strong", "config": f"cfg5 quarter ring p={p} n_el={n_el}, xi3 slabs x{world}",
+            "N": space.n_dofs, "iterations": rep.iterations, "converged": rep.converged,
+            "final_rel_residual": rep.residuals[-1], "solve_s": secs, "setup_s": setup_s,
+            "rule_s": t1 - t0, "u_norm": float(nrm[0]) ** 0.5, "device_memory_used_gb": (total - free) / 1e9,
+            "solver": "mfwq_pcg_solve_comm (NCCL)" if world > 1 else "mfwq_pcg_solve (single GPU)"}
 
 
 def solve_case(M, torch, dev, p, n_el, geom="ring", reps=1, otf=False):
@@ -678,21 +762,59 @@ def dropin_e2e(torch, ops, dofs_step, steps):
             "h2d_bytes_per_step": 8 * dofs_step, "d2h_bytes_per_step": 8 * dofs_step, "steps": n}
 
 
+def run_slab_headline(args, rank, world, local):
+    """N > 1: the headline is the cfg5 slab PCG on N GPUs (strong scaling; one rank per GPU, NCCL)."""
+    import torch
+
+    import paper_1712_08565_b200 as M
+    from paper_1712_08565_b200 import _lib
+    dev = torch.device("cuda", local)
+    launches0 = _lib.lib().mfwq_launch_count()
+    with ClockSampler(local) as clk:
+        r = run_slab_pcg(M, torch, dev, rank, world, steps=args.steps, warmup=args.warmup)
+    launches = _lib.lib().mfwq_launch_count() - launches0
+    if rank == 0:
+        line = {"metric": SLAB_METRIC, "value": r["value"], "unit": r["unit"], "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * r["solve_s"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": r["config"], "parallelism": f"xi3 slabs x{world} (NCCL)"},
+                "slab_pcg": r, "gpu_launches": int(launches), "clocks": clk.summary(),
+                "note": "N=1 lines carry the same cfg5 solve on one GPU under 'slab_pcg' (the strong-scaling "
+                        "baseline); the single-GPU headline is the cfg2 matvec sweep"}
+        print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) through torch.distributed.run."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     rank, world, local = dist_info()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        if world > 1 and args.slab:
+            run_reference_slab(args, rank, world)
+        else:
+            run_reference(args, rank, world)
         return
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    run_ours(args, rank, world, local)
-    if world > 1:
-        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_slab_headline(args, rank, world, local)
         dist.destroy_process_group()
+        return
+    run_ours(args, rank, world, local)
 
 
 if __name__ == "__main__":

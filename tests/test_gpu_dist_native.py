@@ -98,3 +98,23 @@ def test_native_slab_pcg_nccl_one_rank():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_native_slab_pcg_cfg5_one_vs_eight():
+    """cfg 5 (quarter ring p = 6, n_el = 512, 137 M DoFs): the single-GPU device PCG against the same
+    solve split into 8 emulated ranks (its only parity route: the CPU reference cannot run cfg 5)."""
+    import gc
+    space = M.tensor_space(6, 512)
+    rule = M.build_tensor_rule(space)
+    geom = M.quarter_ring_map()
+    b = torch.from_numpy(np.random.default_rng(1).standard_normal(space.n_dofs)).cuda()
+    A = M.setup_stiffness(space, rule, geom)
+    P = M.FDPreconditioner(space)
+    u1, r1 = M.cg(A.apply, b, P.apply, tol=1e-8)
+    u1 = u1.cpu()
+    del A, P
+    gc.collect()
+    torch.cuda.empty_cache()
+    uP, rP = _solve(space, rule, geom, 8, b)
+    assert r1.converged and rP.converged and abs(rP.iterations - r1.iterations) <= 1, (rP.iterations, r1.iterations)
+    assert float(torch.linalg.vector_norm(uP.cpu() - u1) / torch.linalg.vector_norm(u1)) <= 1e-9

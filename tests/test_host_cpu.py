@@ -140,3 +140,29 @@ def test_bench_reference_arm_runs_on_host_cores():
     assert line["cpu_baseline"]["cores"] == 2 and line["cpu_baseline"]["kind"] == "port"
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
     assert set(line["per_degree_s"]) == {"2", "3"}
+
+
+def test_bench_reference_arm_slab_headline_under_torchrun():
+    """bench.py --impl reference at N = 2 (launched like the driver does, through torchrun): rank 0
+    times the oracle's PCG iteration on a z-slab sample of the cfg5 problem and prints one line with the
+    N > 1 headline's metric; rank 1 exits 0 without work."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, MFWQ_SLAB_SAMPLE_NXY="6", MFWQ_SLAB_SAMPLE_EL="2")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["scaling"] == "strong" and line["value"] > 0
+    assert line["metric"].startswith("MF-WQ cfg5 slab FD-PCG") and line["e2e"]["value"] == line["value"]
