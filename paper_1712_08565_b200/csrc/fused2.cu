@@ -933,7 +933,7 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
       const int E = S.e_hi - S.e_lo;
       int chunk = E + (E & 1);
       double best = 1e300;
-      for (int nch = 1; nch <= std::max(1, E / 4); ++nch) {
+      for (int nch = 1; nch <= std::max(1, E / 2); ++nch) {
         int len = (E + nch - 1) / nch;
         len += len & 1;
         const long long ctas = inplane * ((E + len - 1) / len);

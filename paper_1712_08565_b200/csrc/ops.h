@@ -47,6 +47,7 @@ class Stiffness {
 
   DevBuf<double> pcg_ws;  // PCG work vectors (r, z, p, Ap) + reduction partials, reused across solves
   DevBuf<double> dist_ws;  // slab-distributed PCG workspace of this rank (dist.cu)
+  std::shared_ptr<void> pcg_graphs;  // captured PCG iteration bodies (pcg.cu)
 
   // on-the-fly coefficients (operators.py:171-183, 207-220): for the analytic maps C depends on
   // xi1 at most, so the kernel reads C(xi1) from a [6][m1] table instead of 6 N_q grids

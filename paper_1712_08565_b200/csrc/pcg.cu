@@ -3,6 +3,7 @@
 // reads back two scalars (p.Ap and ||r||^2) for the indefiniteness and
 // stopping tests, exactly where the reference takes those decisions.
 #include <cmath>
+#include <functional>
 #include <cstdint>
 
 #include "ops.h"
@@ -140,73 +141,77 @@ double dev_dot(const double* a, const double* b, long long N, cudaStream_t s) {
   return h;
 }
 
+// Graph cache of one (operator, preconditioner) pair: the PCG iteration bodies captured once and
+// replayed, so a solve issues a handful of graph launches instead of ~20 kernel launches per
+// iteration (the small-problem solve is launch-latency bound: cfg 1).  Captured after a first
+// eager solve has created every plan, scratch buffer and tensor map the bodies touch.
+struct PcgGraphs {
+  FastDiag* P = nullptr;
+  long long N = 0;
+  const double* ws = nullptr;
+  const double* hslot = nullptr;
+  int device = -1;
+  cudaStream_t cs = nullptr;  // capture stream (the caller's may be the legacy default stream)
+  cudaGraphExec_t init = nullptr, full = nullptr, aonly = nullptr, ponly = nullptr;
+  long long nk_init = 0, nk_full = 0, nk_a = 0, nk_p = 0;
+  bool ready = false;
+  ~PcgGraphs() {
+    for (cudaGraphExec_t g : {init, full, aonly, ponly})
+      if (g) cudaGraphExecDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+  }
+};
+
+static cudaGraphExec_t capture(cudaStream_t cs, long long& nk, const std::function<void()>& body) {
+  const long long c0 = __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
+  MFWQ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(cs, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  MFWQ_CUDA(cudaStreamEndCapture(cs, &g));
+  nk = __atomic_load_n(&g_launches, __ATOMIC_RELAXED) - c0;
+  __atomic_sub_fetch(&g_launches, nk, __ATOMIC_RELAXED);  // captured, not launched
+  cudaGraphExec_t e = nullptr;
+  const cudaError_t err = cudaGraphInstantiate(&e, g, 0);
+  cudaGraphDestroy(g);
+  MFWQ_CUDA(err);
+  return e;
+}
+
+static void replay(cudaGraphExec_t g, long long nk, cudaStream_t s) {
+  MFWQ_CUDA(cudaGraphLaunch(g, s));
+  __atomic_add_fetch(&g_launches, nk, __ATOMIC_RELAXED);
+}
+
 void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long N, double tol, int maxit,
                std::vector<double>& hist, KrylovOut& out, cudaStream_t s) {
   hist.clear();
   out = KrylovOut{};
-  MFWQ_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s));
-  // persistent workspace on the operator (no cudaMalloc/cudaFree inside the solve)
-  // work vectors at a 32-double pitch: every one 256-byte aligned for the 16-byte update kernels
+  // persistent workspace on the operator (no cudaMalloc/cudaFree inside the solve), work vectors at
+  // a 32-double pitch (256-byte aligned for the 16-byte update kernels); the iterate x lives in the
+  // workspace too and is copied to the caller's buffer at the end, so the captured bodies never see
+  // a caller pointer
   const long long NP = (N + 31) & ~31LL;
-  const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  A.pcg_ws.alloc_at_least(x_aligned ? 4 * NP + RGRID + 4 : 5 * NP + 640);
+  A.pcg_ws.alloc_at_least(5 * NP + RGRID + 32);
   double* r = A.pcg_ws.ptr;
   double* z = r + NP;
   double* p = z + NP;
   double* Ap = p + NP;
-  double* const x_out = x;
-  if (!x_aligned) {  // iterate in an aligned copy, hand the result back at the end
-    x = r + 4 * NP + 640;  // 32-double aligned slot after the partials and scalars
-    MFWQ_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s));
-  }
-  struct CopyBack {
-    double* dst;
-    const double* src;
-    long long n;
-    cudaStream_t s;
-    ~CopyBack() {
-      if (dst != src) cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
-    }
-  } copy_back{x_out, x, N, s};
-  struct { double* ptr; } part{Ap + NP}, sc{Ap + NP + RGRID};  // sc: 0 rz, 1 pAp, 2 rr, 3 rz_new
-  double* rz = sc.ptr;
-  double* pAp = sc.ptr + 1;
-  double* rr = sc.ptr + 2;
-  double* rzn = sc.ptr + 3;
-  dot_to(b, b, N, part.ptr, rr, s);
-  double h2[2];
-  MFWQ_CUDA(cudaMemcpyAsync(h2, rr, sizeof(double), cudaMemcpyDeviceToHost, s));
-  MFWQ_CUDA(cudaStreamSynchronize(s));
-  const double bnorm = std::sqrt(h2[0]);
-  if (bnorm == 0.0) {  // solvers.py:142-143
-    hist.push_back(0.0);
-    out.converged = 1;
-    return;
-  }
-  MFWQ_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  if (P) P->apply(r, z, s);
-  else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  out.precs = 1;
-  MFWQ_CUDA(cudaMemcpyAsync(p, z, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  dot_to(r, z, N, part.ptr, rz, s);
-  hist.push_back(1.0);
-  // The next preconditioner apply (and its r.z / p update) is enqueued BEFORE the host reads the
-  // iteration's scalars whenever the last residual is far above tol: the device then never idles
-  // through the host round trip.  The arithmetic and its order are unchanged; on a (rare) wrong
-  // guess the extra work is simply dropped (counters count only what the reference would do).
-  bool ahead = false;  // P(r), r.z, p-update of this iteration already enqueued
-  double last_rel = 1.0;
-  auto enqueue_precond = [&]() {
-    if (P) P->apply(r, z, s);
-    else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    dot_to(r, z, N, part.ptr, rzn, s);
-    update_p<<<RGRID, RB, 0, s>>>(p, z, N, rzn, rz); note_launch();
-    copy_scalar<<<1, 1, 0, s>>>(rzn, rz); note_launch();
-    MFWQ_CUDA(cudaGetLastError());
-  };
-  // pinned landing slot for the two scalars and the event marking their arrival: created once per
-  // host thread (cudaMallocHost costs ~1 ms, far more than a small solve)
-  // host thread; the event belongs to a device, so there is one per device the thread solves on
+  double* xw = Ap + NP;
+  double* part = xw + NP;
+  double* sc = part + RGRID;  // 0 rz, 1 pAp, 2 rr, 3 rz_new
+  double* rz = sc;
+  double* pAp = sc + 1;
+  double* rr = sc + 2;
+  double* rzn = sc + 3;
+  // pinned landing slot for the scalars and the event marking their arrival: created once per host
+  // thread; the event belongs to a device, so there is one per device the thread solves on
   constexpr int MAXDEV = 64;
   struct ScalarSlot {
     cudaEvent_t ev[64] = {};
@@ -221,46 +226,141 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
   int cur_dev = 0;
   MFWQ_CUDA(cudaGetDevice(&cur_dev));
   if (cur_dev < 0 || cur_dev >= MAXDEV) throw ValueErr("device index out of range");
-  if (!slot.h) MFWQ_CUDA(cudaMallocHost(&slot.h, 2 * sizeof(double)));
+  if (!slot.h) MFWQ_CUDA(cudaMallocHost(&slot.h, 4 * sizeof(double)));
   if (!slot.ev[cur_dev]) MFWQ_CUDA(cudaEventCreateWithFlags(&slot.ev[cur_dev], cudaEventDisableTiming));
   cudaEvent_t ev = slot.ev[cur_dev];
   double* hsc = slot.h;
-  for (int k = 1; k <= maxit; ++k) {
-    A.apply(p, Ap, s);
-    out.matvecs++;
-    dot_to(p, Ap, N, part.ptr, pAp, s);
-    update_xr<<<RGRID, RB, 0, s>>>(x, r, p, Ap, N, rz, pAp, part.ptr); note_launch();
-    finish_sum<<<1, RB, 0, s>>>(part.ptr, RGRID, rr); note_launch();
+
+  // the host-visible event: an external event node when the body is being captured
+  bool capturing = false;
+  auto record = [&](cudaStream_t t) {
+    if (capturing) MFWQ_CUDA(cudaEventRecordWithFlags(ev, t, cudaEventRecordExternal));
+    else MFWQ_CUDA(cudaEventRecord(ev, t));
+  };
+  // the iteration bodies (each enqueued on stream t)
+  auto body_init = [&](cudaStream_t t) {  // z = P r, p = z, rz = r.z  (solvers.py:147-151)
+    if (P) P->apply(r, z, t);
+    else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, t));
+    MFWQ_CUDA(cudaMemcpyAsync(p, z, N * sizeof(double), cudaMemcpyDeviceToDevice, t));
+    dot_to(r, z, N, part, rz, t);
+    MFWQ_CUDA(cudaMemcpyAsync(hsc + 2, rr, sizeof(double), cudaMemcpyDeviceToHost, t));  // ||b||^2
+    record(t);
+  };
+  auto body_a = [&](cudaStream_t t) {  // Ap, p.Ap, x / r update, ||r||^2 -> host (solvers.py:154-165)
+    A.apply(p, Ap, t);
+    dot_to(p, Ap, N, part, pAp, t);
+    update_xr<<<RGRID, RB, 0, t>>>(xw, r, p, Ap, N, rz, pAp, part); note_launch();
+    finish_sum<<<1, RB, 0, t>>>(part, RGRID, rr); note_launch();
     MFWQ_CUDA(cudaGetLastError());
-    MFWQ_CUDA(cudaMemcpyAsync(hsc, pAp, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    MFWQ_CUDA(cudaEventRecord(ev, s));
-    // PCG reduces the residual by a bounded factor per step: far from tol, the next step is certain
-    ahead = k < maxit && last_rel > 1e3 * tol;
-    if (ahead) enqueue_precond();
+    MFWQ_CUDA(cudaMemcpyAsync(hsc, pAp, 2 * sizeof(double), cudaMemcpyDeviceToHost, t));
+    record(t);
+  };
+  auto body_p = [&](cudaStream_t t) {  // z = P r, p = z + beta p  (solvers.py:168-172)
+    if (P) P->apply(r, z, t);
+    else MFWQ_CUDA(cudaMemcpyAsync(z, r, N * sizeof(double), cudaMemcpyDeviceToDevice, t));
+    dot_to(r, z, N, part, rzn, t);
+    update_p<<<RGRID, RB, 0, t>>>(p, z, N, rzn, rz); note_launch();
+    copy_scalar<<<1, 1, 0, t>>>(rzn, rz); note_launch();
+    MFWQ_CUDA(cudaGetLastError());
+  };
+
+  // graphs: built after the first eager solve of this (A, P) pair on this device and host slot
+  auto* G = static_cast<PcgGraphs*>(A.pcg_graphs.get());
+  const bool graphs_ok = !getenv("MFWQ_NO_PCG_GRAPHS");
+  const bool use_graphs = graphs_ok && G && G->ready && G->P == P && G->N == N && G->ws == A.pcg_ws.ptr &&
+                          G->hslot == hsc && G->device == cur_dev;
+
+  MFWQ_CUDA(cudaMemsetAsync(xw, 0, N * sizeof(double), s));
+  MFWQ_CUDA(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  dot_to(b, b, N, part, rr, s);
+  // the preconditioner of the first step runs before ||b|| is known on the host: if b = 0 it only
+  // produces zeros, which are discarded (solvers.py:142-143 returns before P is applied)
+  if (use_graphs) replay(G->init, G->nk_init, s);
+  else body_init(s);
+  MFWQ_CUDA(cudaEventSynchronize(ev));
+  const double bnorm = std::sqrt(hsc[2]);
+  auto finish = [&]() {
+    MFWQ_CUDA(cudaMemcpyAsync(x, xw, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MFWQ_CUDA(cudaStreamSynchronize(s));
+  };
+  if (bnorm == 0.0) {
+    hist.push_back(0.0);
+    out.converged = 1;
+    finish();
+    return;
+  }
+  out.precs = 1;
+  hist.push_back(1.0);
+  // The next preconditioner apply (and its r.z / p update) is enqueued BEFORE the host reads the
+  // iteration's scalars whenever the last residual is far above tol: the device then never idles
+  // through the host round trip.  The arithmetic and its order are unchanged; on a (rare) wrong
+  // guess the extra work is simply dropped (counters count only what the reference would do).
+  double last_rel = 1.0;
+  bool done = false;
+  for (int k = 1; k <= maxit && !done; ++k) {
+    const bool ahead = k < maxit && last_rel > 1e3 * tol;
+    if (use_graphs) replay(ahead ? G->full : G->aonly, ahead ? G->nk_full : G->nk_a, s);
+    else {
+      body_a(s);
+      if (ahead) body_p(s);
+    }
+    out.matvecs++;
     MFWQ_CUDA(cudaEventSynchronize(ev));
-    h2[0] = hsc[0];
-    h2[1] = hsc[1];
-    if (h2[0] <= 0) {  // solvers.py:156-160
+    const double pap = hsc[0], rrv = hsc[1];
+    if (pap <= 0) {  // solvers.py:156-160
       char m[128];
-      snprintf(m, sizeof m, "nonpositive curvature p.Ap = %.3e at iteration %d", h2[0], k);
+      snprintf(m, sizeof m, "nonpositive curvature p.Ap = %.3e at iteration %d", pap, k);
       MFWQ_CUDA(cudaStreamSynchronize(s));
       throw IndefiniteErr(m);
     }
-    const double rel = std::sqrt(h2[1]) / bnorm;
+    const double rel = std::sqrt(rrv) / bnorm;
     hist.push_back(rel);
     last_rel = rel;
     if (rel <= tol) {
-      MFWQ_CUDA(cudaStreamSynchronize(s));  // a speculative step may still be running on x's stream
       out.iterations = k;
       out.converged = 1;
-      return;
+      done = true;
+      break;
     }
-    if (!ahead) enqueue_precond();
+    if (!ahead) {
+      if (use_graphs) replay(G->ponly, G->nk_p, s);
+      else body_p(s);
+    }
     out.precs++;
   }
-  MFWQ_CUDA(cudaStreamSynchronize(s));
-  out.iterations = maxit;
-  out.converged = 0;
+  if (!done) {
+    out.iterations = maxit;
+    out.converged = 0;
+  }
+  finish();
+  if (graphs_ok && !use_graphs && !(G && G->N == -1)) {  // capture the bodies for the next solve of this pair
+    auto* NG = new PcgGraphs();
+    A.pcg_graphs = std::shared_ptr<void>(NG, [](void* q) { delete static_cast<PcgGraphs*>(q); });
+    NG->P = P;
+    NG->N = N;
+    NG->ws = A.pcg_ws.ptr;
+    NG->hslot = hsc;
+    NG->device = cur_dev;
+    try {  // an operator path that cannot be captured keeps solving eagerly (the solve above is done)
+      MFWQ_CUDA(cudaStreamCreateWithFlags(&NG->cs, cudaStreamNonBlocking));
+      capturing = true;
+      NG->init = capture(NG->cs, NG->nk_init, [&] { body_init(NG->cs); });
+      NG->aonly = capture(NG->cs, NG->nk_a, [&] { body_a(NG->cs); });
+      NG->ponly = capture(NG->cs, NG->nk_p, [&] { body_p(NG->cs); });
+      NG->full = capture(NG->cs, NG->nk_full, [&] {
+        body_a(NG->cs);
+        body_p(NG->cs);
+      });
+      NG->ready = true;
+      capturing = false;
+    } catch (const std::exception&) {
+      capturing = false;
+      cudaGetLastError();  // clear a sticky capture error
+      NG->ready = false;
+      NG->P = nullptr;
+      NG->N = -1;  // never matches: this pair stays eager
+    }
+  }
 }
 
 }  // namespace mfwq
