@@ -81,6 +81,7 @@ struct Params {
   int nel3;
   int qe;              // max quadrature planes per z-element
   const double* C;     // 6 grids (padded pitch m1p)
+  const double* Cm;    // the mass term's alpha det J grid (same layout), or null
   size_t gstride;
   int m1p;
   const double* x;
@@ -100,19 +101,24 @@ struct Params {
 };
 
 
+// coefficient grids: the six symmetric C_ab (a <= b) and, for the mass term, alpha det J
+constexpr int NGRID = 7, MASS_GRID = 6, MASS_TERM = 0x200;
+
 struct Maps {
-  CUtensorMap m[12];  // per coefficient grid: 16 x 16 x 4 boxes, then 16 x 16 x 2 boxes (zero fill past the grid edge)
+  CUtensorMap m[2 * NGRID];  // per coefficient grid: 16 x 16 x 4 boxes, then 16 x 16 x 2 boxes (zero fill past the grid edge)
 };
 
 // Term set KS: bit 3a+b set when the term (a,b) runs in this kernel (0x111 diagonal C, 0x11B the
 // stored quarter ring's diagonal + C01, 0x1FF general); the t-th term is the t-th set bit.
+// bits 0..8: the stiffness terms (a,b); bit 9: the mass term (B0 / W00 in every direction, the
+// alpha det J grid; operators.py:87-132), coded as (a, b) = (3, 3)
 __host__ __device__ constexpr int popc9(int ks) {
   int n = 0;
-  for (int i = 0; i < 9; ++i) n += (ks >> i) & 1;
+  for (int i = 0; i < 10; ++i) n += (ks >> i) & 1;
   return n;
 }
 __host__ __device__ constexpr int nth_bit(int ks, int t) {
-  for (int i = 0; i < 9; ++i)
+  for (int i = 0; i < 10; ++i)
     if ((ks >> i) & 1) {
       if (t == 0) return i;
       --t;
@@ -125,16 +131,18 @@ struct Terms {
   // bit index of term t, tabulated once (a(t) / b(t) fold to constants in the unrolled loops)
   static constexpr int I0 = nth_bit(KS, 0), I1 = nth_bit(KS, 1), I2 = nth_bit(KS, 2), I3 = nth_bit(KS, 3),
                        I4 = nth_bit(KS, 4), I5 = nth_bit(KS, 5), I6 = nth_bit(KS, 6), I7 = nth_bit(KS, 7),
-                       I8 = nth_bit(KS, 8);
+                       I8 = nth_bit(KS, 8), I9 = nth_bit(KS, 9);
   __host__ __device__ static constexpr int idx(int t) {
-    return t == 0 ? I0 : t == 1 ? I1 : t == 2 ? I2 : t == 3 ? I3 : t == 4 ? I4 : t == 5 ? I5 : t == 6 ? I6 : t == 7 ? I7 : I8;
+    return t == 0 ? I0 : t == 1 ? I1 : t == 2 ? I2 : t == 3 ? I3 : t == 4 ? I4 : t == 5 ? I5 : t == 6 ? I6 : t == 7 ? I7 : t == 8 ? I8 : I9;
   }
-  __host__ __device__ static constexpr int a(int t) { return idx(t) / 3; }
-  __host__ __device__ static constexpr int b(int t) { return idx(t) % 3; }
+  __host__ __device__ static constexpr int a(int t) { return idx(t) == 9 ? 3 : idx(t) / 3; }
+  __host__ __device__ static constexpr int b(int t) { return idx(t) == 9 ? 3 : idx(t) % 3; }
 };
-// symmetric grid index of (a,b): 00,01,02,11,12,22 -> 0..5 (non-recursive so it folds after unrolling)
+// symmetric grid index of (a,b): 00,01,02,11,12,22 -> 0..5, the mass term (3,3) -> 6
+// (non-recursive so it folds after unrolling)
 __host__ __device__ constexpr int gkey(int a, int b) {
-  return (a < b ? a : b) == 0 ? (a < b ? b : a) : ((a < b ? a : b) == 1 ? 2 + (a < b ? b : a) : 5);
+  return a == 3 ? MASS_GRID
+                : (a < b ? a : b) == 0 ? (a < b ? b : a) : ((a < b ? a : b) == 1 ? 2 + (a < b ? b : a) : 5);
 }
 __host__ __device__ constexpr int wtype(int a, int b, int l) { return 2 * (a == l) + (b == l); }
 template <int KS>
@@ -146,7 +154,7 @@ __host__ __device__ constexpr bool grid_used(int g) {
 template <int KS>
 __host__ __device__ constexpr int n_grids() {
   int n = 0;
-  for (int g = 0; g < 6; ++g) n += grid_used<KS>(g) ? 1 : 0;
+  for (int g = 0; g < NGRID; ++g) n += grid_used<KS>(g) ? 1 : 0;
   return n;
 }
 template <int KS>
@@ -222,7 +230,10 @@ __host__ __device__ constexpr int zs_for(int p, int ks) {
   return (ks == 0x11B && p == 3) ? 1 : 2;
 }
 __host__ __device__ constexpr int occ_for(int p, int ks) {
-  return ks == 0x111 ? (p <= 6 ? 2 : 1) : ks == 0x11B ? ((p <= 2 || zs_for(p, ks) == 1) ? 2 : 1) : 1;
+  return ks == 0x111 ? (p <= 6 ? 2 : 1)
+         : ks == 0x11B ? ((p <= 2 || zs_for(p, ks) == 1) ? 2 : 1)
+         : ks == 0x200 ? 2  // the mass term: one ring, one accumulator set
+                       : 1;
 }
 // gradient components the term set needs (b of its terms)
 template <int KS>
@@ -294,6 +305,7 @@ struct Smem {
 
 template <int P, int KS, int ZS, bool OTF>
 __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) {
+  static_assert(!(OTF && (KS & MASS_TERM)), "the mass term runs on its stored alpha det J grid");
   using L = Smem<P, KS, ZS, OTF>;
   constexpr int NT = Terms<KS>::N;
   constexpr int NB = L::NB, NW = L::NW, NBP = L::NBP, NWP = L::NWP, ZT = L::ZT, G = L::G;
@@ -434,9 +446,9 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
       const int sl = warp - 1;
       int g = 0;
 #pragma unroll
-      for (int h = 0; h < 6; ++h)
+      for (int h = 0; h < NGRID; ++h)
         if (grid_used<KS>(h) && grid_slot<KS>(h) == sl) g = h;
-      tma_load_3d(sC + sl * (2 * ZS) * 256, &maps.m[(ZS == 2 ? 0 : 6) + g], sInf->q0x, sInf->q0y, qa - prm.qzb, &mbar[0]);
+      tma_load_3d(sC + sl * (2 * ZS) * 256, &maps.m[(ZS == 2 ? 0 : NGRID) + g], sInf->q0x, sInf->q0y, qa - prm.qzb, &mbar[0]);
     }
   };
   // a step takes its coefficients by TMA when it has ZS elements of exactly 2 planes each
@@ -457,7 +469,7 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
 #pragma unroll
     for (int k = 0; k < NB; ++k) {  // only the gradient components the term set uses
       if constexpr (bused<KS>(0)) vx = fma(b1[k], a0[k], vx);
-      if constexpr (bused<KS>(2)) v0 = fma(b0[k], a0[k], v0);
+      if constexpr (bused<KS>(2) || bused<KS>(3)) v0 = fma(b0[k], a0[k], v0);
       if constexpr (bused<KS>(1)) vy = fma(b0[k], a1[k], vy);
     }
 #pragma unroll
@@ -472,7 +484,7 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
   };
   // B side, in-plane: DMMA y-contraction of nz planes of sV -> sA
   // By types needed: 0 (By) for the x- and z-gradients, 1 (dBy) for the y-gradient
-  constexpr bool kA0 = bused<KS>(0) || bused<KS>(2), kA1 = bused<KS>(1);
+  constexpr bool kA0 = bused<KS>(0) || bused<KS>(2) || bused<KS>(3), kA1 = bused<KS>(1);
   constexpr int NBY = (kA0 ? 1 : 0) + (kA1 ? 1 : 0);
   auto bside_y = [&](int nz) {
     for (int task = warp; task < ((MFWQ_ABLATE == 2 || (MFWQ_ABL_MASK & 1)) ? 0 : NBY * 2 * NTD); task += NWARP) {  // (b, mt, nt)
@@ -586,7 +598,7 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
     const double2* zb0 = reinterpret_cast<const double2*>(zrow);
     const double2* zb1 = reinterpret_cast<const double2*>(zrow + NBP);
     const double2* zw = reinterpret_cast<const double2*>(zrow + 2 * NBP);
-    double gx = 0.0, gy = 0.0, gz = 0.0;
+    double gx = 0.0, gy = 0.0, gz = 0.0, gm = 0.0;
 #pragma unroll
     for (int k2 = 0; k2 < NBP / 2; ++k2) {
       const double2 c0 = zb0[k2], c1 = zb1[k2];
@@ -594,28 +606,30 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
       if constexpr (bused<KS>(0)) gx = fma(c0.x, hx[ro + k], gx);
       if constexpr (bused<KS>(1)) gy = fma(c0.x, hy[ro + k], gy);
       if constexpr (bused<KS>(2)) gz = fma(c1.x, h0[ro + k], gz);
+      if constexpr (bused<KS>(3)) gm = fma(c0.x, h0[ro + k], gm);
       if (k + 1 < NB) {
         if constexpr (bused<KS>(0)) gx = fma(c0.y, hx[ro + k + 1], gx);
         if constexpr (bused<KS>(1)) gy = fma(c0.y, hy[ro + k + 1], gy);
         if constexpr (bused<KS>(2)) gz = fma(c1.y, h0[ro + k + 1], gz);
+        if constexpr (bused<KS>(3)) gm = fma(c0.y, h0[ro + k + 1], gm);
       }
     }
     if (MFWQ_ABLATE == 3) return;
     // inactive lanes (outside a narrow tile) run the same code with zero coefficients: no
     // divergent exit, so the accumulator registers need no reconciling moves
-    double cg[6];
+    double cg[NGRID];
 #pragma unroll
-    for (int g = 0; g < 6; ++g) {
+    for (int g = 0; g < NGRID; ++g) {
       if (!grid_used<KS>(g)) { cg[g] = 0.0; continue; }
       if constexpr (OTF) cg[g] = active ? sCx[grid_slot<KS>(g) * TQ + ql1] : 0.0;
       else if constexpr (kTMA) cg[g] = active ? cst[grid_slot<KS>(g) * (2 * ZS) * 256] : 0.0;
-      else cg[g] = active ? __ldg(prm.C + g * prm.gstride + ((size_t)(qz - prm.qzb) * prm.m[1] + sInf->q0y + ql2) * prm.m1p + sInf->q0x + ql1) : 0.0;
+      else cg[g] = active ? __ldg((g == MASS_GRID ? prm.Cm : prm.C + g * prm.gstride) + ((size_t)(qz - prm.qzb) * prm.m[1] + sInf->q0y + ql2) * prm.m1p + sInf->q0x + ql1) : 0.0;
     }
     double tv[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int b = T::b(t);
-      tv[t] = cg[gkey(T::a(t), b)] * (b == 0 ? gx : (b == 1 ? gy : gz));
+      tv[t] = cg[gkey(T::a(t), b)] * (b == 0 ? gx : (b == 1 ? gy : (b == 2 ? gz : gm)));
     }
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -643,9 +657,9 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
   // eighteen-odd two-deep accumulator chains in flight instead of one plane's dependent sequence.
   // zr: the plane-0 row of the z table (plane 1 follows at zs doubles).
   auto zelem = [&](const double* zr, int zs, const double* cst) {
-    double g[2][3];
+    double g[2][4];
 #pragma unroll
-    for (int pl = 0; pl < 2; ++pl) g[pl][0] = g[pl][1] = g[pl][2] = 0.0;
+    for (int pl = 0; pl < 2; ++pl) g[pl][0] = g[pl][1] = g[pl][2] = g[pl][3] = 0.0;
 #pragma unroll
     for (int k2 = 0; k2 < NBP / 2; ++k2)
 #pragma unroll
@@ -656,18 +670,20 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
         if constexpr (bused<KS>(0)) g[pl][0] = fma(c0.x, hx[k], g[pl][0]);
         if constexpr (bused<KS>(1)) g[pl][1] = fma(c0.x, hy[k], g[pl][1]);
         if constexpr (bused<KS>(2)) g[pl][2] = fma(c1.x, h0[k], g[pl][2]);
+        if constexpr (bused<KS>(3)) g[pl][3] = fma(c0.x, h0[k], g[pl][3]);
         if (k + 1 < NB) {
           if constexpr (bused<KS>(0)) g[pl][0] = fma(c0.y, hx[k + 1], g[pl][0]);
           if constexpr (bused<KS>(1)) g[pl][1] = fma(c0.y, hy[k + 1], g[pl][1]);
           if constexpr (bused<KS>(2)) g[pl][2] = fma(c1.y, h0[k + 1], g[pl][2]);
+          if constexpr (bused<KS>(3)) g[pl][3] = fma(c0.y, h0[k + 1], g[pl][3]);
         }
       }
     double tv[2][NT];
 #pragma unroll
     for (int pl = 0; pl < 2; ++pl) {
-      double cg[6];
+      double cg[NGRID];
 #pragma unroll
-      for (int gg = 0; gg < 6; ++gg) {
+      for (int gg = 0; gg < NGRID; ++gg) {
         if (!grid_used<KS>(gg)) { cg[gg] = 0.0; continue; }
         if constexpr (OTF) cg[gg] = active ? sCx[grid_slot<KS>(gg) * TQ + ql1] : 0.0;
         else cg[gg] = active ? cst[pl * 256 + grid_slot<KS>(gg) * (2 * ZS) * 256] : 0.0;
@@ -837,6 +853,7 @@ struct Fused2Plan {
   int ntile[3] = {0, 0, 0};
   int max_nqz = 0, qe = 0, max_chunk = 0;
   const double* maps_for = nullptr;  // coefficient buffer the maps were encoded for
+  const double* maps_for_mass = nullptr;  // mass grid the mass maps were encoded for
   f2::Maps maps;  // 16 x 16 x 4 / x 2 boxes: the ZS x 2 planes of a regular step
 };
 
@@ -1025,21 +1042,24 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 void encode_maps(Stiffness& S, Fused2Plan& F) {
-  if (F.maps_for == S.coeff.ptr) return;
+  if (F.maps_for == S.coeff.ptr && F.maps_for_mass == S.mass_grid.ptr) return;
   auto enc = get_encode();
   const size_t G = S.grid_elems();
-  for (int mi = 0; mi < 12; ++mi) {
-    const int g = mi % 6;
+  for (int mi = 0; mi < 2 * f2::NGRID; ++mi) {
+    const int g = mi % f2::NGRID;
+    const double* base = g == f2::MASS_GRID ? S.mass_grid.ptr : (S.coeff.ptr ? S.coeff.ptr + g * G : nullptr);
+    if (!base) continue;  // a grid this operator does not hold is never read
     cuuint64_t dims[3] = {(cuuint64_t)S.dir[0].m, (cuuint64_t)S.dir[1].m, (cuuint64_t)(S.q_hi - S.q_lo)};
     cuuint64_t strides[2] = {(cuuint64_t)S.m1p * 8, (cuuint64_t)S.m1p * S.dir[1].m * 8};
-    cuuint32_t box[3] = {(cuuint32_t)f2::TQ, (cuuint32_t)f2::TQ, mi < 6 ? 4u : 2u};  // the ZS x 2 planes of a step
+    cuuint32_t box[3] = {(cuuint32_t)f2::TQ, (cuuint32_t)f2::TQ, mi < f2::NGRID ? 4u : 2u};  // the ZS x 2 planes of a step
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&F.maps.m[mi], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(S.coeff.ptr + g * G), dims,
+    CUresult r = enc(&F.maps.m[mi], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims,
                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaErr("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   }
   F.maps_for = S.coeff.ptr;
+  F.maps_for_mass = S.mass_grid.ptr;
 }
 
 #endif
@@ -1077,6 +1097,7 @@ static void fill_params(Stiffness& S, Fused2Plan& F, const double* x, double* y,
   prm.nty = F.ntile[1];
   prm.nel3 = S.dir[2].n_el;
   prm.C = S.coeff.ptr;
+  prm.Cm = S.mass_grid.ptr;
   prm.gstride = S.grid_elems();
   prm.m1p = S.m1p;
   prm.x = x;
@@ -1174,6 +1195,32 @@ bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s) {
 }
 
 bool fused2_accepts(Stiffness& S) { return fused2_plan(S)->ok; }
+
+// the mass operator (operators.py:87-132) as the fused kernel's one-term case: B0 / W00 in every
+// direction, the stored alpha det J grid; false when the rule is outside the element-blocked
+// structure (the composed K1 path then runs)
+template <int P>
+static void launch_mass(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
+  launch2<P, f2::MASS_TERM, false>(S, F, x, y, s);
+}
+bool fused2_apply_mass(Stiffness& S, const double* x, double* y, cudaStream_t s) {
+  Fused2Plan* F = fused2_plan(S);
+  if (!F->ok || !S.mass_grid.ptr) return false;
+  switch (F->p) {
+    case 1: launch_mass<1>(S, *F, x, y, s); break;
+    case 2: launch_mass<2>(S, *F, x, y, s); break;
+    case 3: launch_mass<3>(S, *F, x, y, s); break;
+    case 4: launch_mass<4>(S, *F, x, y, s); break;
+    case 5: launch_mass<5>(S, *F, x, y, s); break;
+    case 6: launch_mass<6>(S, *F, x, y, s); break;
+    case 7: launch_mass<7>(S, *F, x, y, s); break;
+    case 8: launch_mass<8>(S, *F, x, y, s); break;
+    case 9: launch_mass<9>(S, *F, x, y, s); break;
+    case 10: launch_mass<10>(S, *F, x, y, s); break;
+    default: return false;
+  }
+  return true;
+}
 
 void Stiffness::apply_fused(const double* x, double* y, cudaStream_t s) {
   if (fused2_apply(*this, x, y, s)) return;

@@ -119,6 +119,7 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
 // element-blocked fused matvec (fused2.cu); false when the rule is outside its structure
 bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s);
 bool fused2_accepts(Stiffness& S);  // the rule fits the element-blocked structure (plans it)
+bool fused2_apply_mass(Stiffness& S, const double* x, double* y, cudaStream_t s);  // mass as the one-term case
 
 void kron_apply_dense(int d, const int* rows, const int* cols, const double* const* A, const double* x, double* y,
                       int accumulate, cudaStream_t s);

@@ -549,6 +549,9 @@ void Stiffness::eval_mass(double* out, const double* J_dev, cudaStream_t s) {
 // w = (W00 x W00 x W00)(m o (B0 x B0 x B0) v), contracted direction 3 first (kron.py:83)
 void Stiffness::apply_mass(const double* x, double* y, cudaStream_t s) {
   if (!mass_ready) throw ValueErr("mass coefficients not set");
+  // the fused kernel's one-term case on the stored alpha det J grid; the composed K1 path below
+  // serves on-the-fly mass, path = generic, and rules outside the element-blocked structure
+  if (!mass_otf && path != 1 && fused2_apply_mass(*this, x, y, s)) return;
   const int n1 = dir[0].n, n2 = dir[1].n, n3 = dir[2].n;
   const int m1 = dir[0].m, m2 = dir[1].m, m3 = dir[2].m;
   if (!g_.ptr) {
