@@ -160,8 +160,9 @@ __global__ void coeff_kernel(int kind, const double* __restrict__ x1, const doub
                              double A21, double A22, int kconst, double K00, double K01, double K02,
                              double K10, double K11, double K12, double K20, double K21, double K22,
                              const double* __restrict__ Jfield, const double* __restrict__ Kfield,
-                             double* __restrict__ C, size_t gstride, unsigned long long* bad) {
+                             double* __restrict__ C, size_t gstride, unsigned long long* bad, int* nonzero) {
   const long long Nq = (long long)m1 * m2 * m3;
+  unsigned nzmask = 0;  // grids with a non-zero value at this thread's points (terms to keep, detect_nonzero)
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Nq; q += (long long)gridDim.x * blockDim.x) {
     const int q1 = int(q % m1);
     const long long r = q / m1;
@@ -227,8 +228,16 @@ __global__ void coeff_kernel(int kind, const double* __restrict__ x1, const doub
     for (int g = 0; g < 6; ++g) {
       const int a = keys[g][0], b = keys[g][1];
       const double v = T[a][0] * Ji[b][0] + T[a][1] * Ji[b][1] + T[a][2] * Ji[b][2];
-      C[g * gstride + o] = v * det;
+      const double c = v * det;
+      C[g * gstride + o] = c;
+      if (c != 0.0) nzmask |= 1u << g;
     }
+  }
+  if (nonzero) {  // one atomic per warp and grid that saw a non-zero value
+    nzmask = __reduce_or_sync(0xffffffffu, nzmask);
+    if ((threadIdx.x & 31) == 0)
+      for (int g = 0; g < 6; ++g)
+        if (nzmask >> g & 1) atomicOr(nonzero + g, 1);
   }
 }
 
@@ -256,6 +265,8 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
   DevBuf<unsigned long long> bad(1);
   unsigned long long init = ~0ull;
   MFWQ_CUDA(cudaMemcpyAsync(bad.ptr, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  flag_.alloc(6);  // which grids are not identically zero, found by the coefficient kernel itself
+  MFWQ_CUDA(cudaMemsetAsync(flag_.ptr, 0, 6 * sizeof(int), s));
   double a[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, k[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
   if (A) std::copy(A, A + 9, a);
   if (K9) std::copy(K9, K9 + 9, k);
@@ -270,14 +281,16 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
   coeff_kernel<<<blocks, 256, 0, s>>>(kind, dir[0].pts_d.ptr, dir[1].pts_d.ptr, dir[2].pts_d.ptr + q_lo, m1, m2, m3, m1p,
                                       a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], K9 ? 1 : 0, k[0], k[1],
                                       k[2], k[3], k[4], k[5], k[6], k[7], k[8], J_dev, Kfield_dev, coeff.ptr, G,
-                                      bad.ptr); note_launch();
+                                      bad.ptr, flag_.ptr); note_launch();
   MFWQ_CUDA(cudaGetLastError());
   if (m1p > m1) {
     pad_zero_kernel<<<148, 256, 0, s>>>(coeff.ptr, m1, m1p, (long long)m2 * m3, G); note_launch();
     MFWQ_CUDA(cudaGetLastError());
   }
   unsigned long long hbad = 0;
+  int hnz[6];
   MFWQ_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, sizeof(hbad), cudaMemcpyDeviceToHost, s));
+  MFWQ_CUDA(cudaMemcpyAsync(hnz, flag_.ptr, sizeof hnz, cudaMemcpyDeviceToHost, s));
   MFWQ_CUDA(cudaStreamSynchronize(s));
   if (hbad != ~0ull) {
     long long q = (long long)hbad;
@@ -288,7 +301,7 @@ void Stiffness::set_geometry(int kind, const double* A, const double* K9, const 
     throw DegenerateErr(msg);
   }
   coeffs_ready = true;
-  detect_nonzero(s);
+  for (int g = 0; g < 6; ++g) grid_nonzero[g] = hnz[g] != 0;
 }
 
 // On-the-fly mode: C(xi1) = C(xi1, 0, 0) by the same formula as the grids (coeff_kernel); for the
@@ -318,7 +331,7 @@ void Stiffness::set_on_the_fly(int kind, const double* A, const double* K9, cuda
   coeff_kernel<<<(m1 + 127) / 128, 128, 0, s>>>(kind, dir[0].pts_d.ptr, zero.ptr, zero.ptr, m1, 1, 1, m1, a[0], a[1],
                                                 a[2], a[3], a[4], a[5], a[6], a[7], a[8], geo_hasK ? 1 : 0, k[0],
                                                 k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], nullptr, nullptr,
-                                                cx.ptr, (size_t)m1, bad.ptr); note_launch();
+                                                cx.ptr, (size_t)m1, bad.ptr, nullptr); note_launch();
   MFWQ_CUDA(cudaGetLastError());
   std::vector<double> h(6 * (size_t)m1);
   unsigned long long hbad = 0;
