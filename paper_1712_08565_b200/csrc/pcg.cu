@@ -298,7 +298,9 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
   double last_rel = 1.0;
   bool done = false;
   for (int k = 1; k <= maxit && !done; ++k) {
-    const bool ahead = k < maxit && last_rel > 1e3 * tol;
+    // not on the first step: an exact preconditioner (identity geometry: FD inverts the WQ
+    // stiffness) converges there, and the speculative apply would be pure waste
+    const bool ahead = k > 1 && k < maxit && last_rel > 1e3 * tol;
     if (use_graphs) replay(ahead ? G->full : G->aonly, ahead ? G->nk_full : G->nk_a, s);
     else {
       body_a(s);
