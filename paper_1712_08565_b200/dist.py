@@ -324,8 +324,9 @@ class Communicator:
         return cls(h)
 
     def __del__(self):
+        import sys
         h = getattr(self, "_h", None)
-        if h is not None:
+        if h is not None and not sys.is_finalizing():  # no NCCL teardown during interpreter exit
             from . import _lib
             if _lib._lib is not None:
                 _lib._lib.mfwq_comm_destroy(h)
