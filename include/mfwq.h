@@ -16,6 +16,7 @@
  *   mfwq_stiffness_set_*   _eval_stiffness_coeffs                      operators.py:64-84
  *   mfwq_stiffness_apply   StiffnessOperator.apply                     operators.py:185-204
  *   mfwq_stiffness_apply_host / _host_join  (same, host buffers, pipelined)  operators.py:185-204
+ *   mfwq_stiffness_apply_pageable          (same, pageable host buffers)     operators.py:185-204
  *   mfwq_stiffness_flops   CostMeter count of one apply                kron.py:90-96, operators.py:199-203
  *   mfwq_fd_create         FDPreconditioner.__init__                   solvers.py:72-101
  *   mfwq_fd_apply          FDPreconditioner.apply                      solvers.py:107-115
@@ -132,6 +133,10 @@ int mfwq_stiffness_apply(mfwq_stiffness_t h, const double* x_dev, double* y_dev,
 int mfwq_stiffness_apply_host(mfwq_stiffness_t h, const double* x_host, double* y_host, void* stream);
 /* make `stream` wait for every outstanding D2H of h's host pipeline */
 int mfwq_stiffness_host_join(mfwq_stiffness_t h, void* stream);
+/* y_host = A x_host on pageable host memory (e.g. numpy arrays), synchronous like the reference's
+   numpy apply (operators.py:185-204): the vectors are staged in chunks through pinned buffers by a
+   pool of host threads, each chunk's host copy overlapping the previous chunk's DMA. */
+int mfwq_stiffness_apply_pageable(mfwq_stiffness_t h, const double* x_host, double* y_host, void* stream);
 /* Multi-GPU slab: restrict the operator to z-elements [e_lo, e_hi).
    Must precede set_geometry/set_coeffs (only the slab's quadrature planes are stored).
    apply() then maps the input window of interior DoF planes [v_lo, v_hi) to the

@@ -1,8 +1,13 @@
 // extern "C" boundary of libmfwq.so (declared in include/mfwq.h).
 #include <dlfcn.h>
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/mfwq.h"
 #include "ops.h"
@@ -30,9 +35,148 @@ struct HostPipe {
     cudaStreamDestroy(d2h);
   }
 };
+// Pageable host memory (a numpy array): the driver stages such copies through its own pinned
+// buffer on one thread (~12 GB/s).  Here the host side of each chunk is copied by a small pool of
+// threads into a pinned slot while the previous chunk's DMA runs.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  // dst <- src (bytes), split across the pool's threads and the caller
+  void copy(void* dst, const void* src, size_t bytes) {
+    const int parts = int(workers_.size()) + 1;
+    if (bytes < (size_t(1) << 20)) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    const size_t per = (bytes / parts + 63) & ~size_t(63);
+    {
+      std::unique_lock<std::mutex> lk(m_);
+      for (int k = 1; k < parts; ++k) {
+        const size_t o = per * k;
+        if (o < bytes) tasks_.push_back({static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                         std::min(per, bytes - o)});
+      }
+      pending_ += tasks_.size();
+    }
+    cv_.notify_all();
+    std::memcpy(dst, src, std::min(per, bytes));
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  struct Task { char* dst; const char* src; size_t n; };
+  CopyPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    const int n = int(std::min(7u, hw / 2));  // + the caller
+    for (int k = 0; k < n; ++k) workers_.emplace_back([this] { run(); });
+  }
+  void run() {
+    for (;;) {
+      Task t;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || !tasks_.empty(); });
+        if (stop_ && tasks_.empty()) return;
+        t = tasks_.back();
+        tasks_.pop_back();
+      }
+      std::memcpy(t.dst, t.src, t.n);
+      std::lock_guard<std::mutex> lk(m_);
+      if (--pending_ == 0) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::vector<Task> tasks_;
+  size_t pending_ = 0;
+  bool stop_ = false;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+};
+
+// synchronous apply on pageable host buffers: chunked H2D through two pinned slots, the kernel,
+// chunked D2H through two pinned slots; host copies of chunk k overlap the DMA of chunk k -+ 1
+struct PageablePipe {
+  static constexpr size_t CHUNK = size_t(4) << 20;  // bytes per slot
+  bool ready = false;
+  cudaStream_t cs = nullptr;  // copy stream
+  double* pin[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {}, kdone = nullptr;
+  DevBuf<double> x, y;
+  ~PageablePipe() {
+    if (!ready) return;
+    for (int k = 0; k < 2; ++k) {
+      cudaFreeHost(pin[k]);
+      cudaEventDestroy(ev[k]);
+    }
+    cudaEventDestroy(kdone);
+    cudaStreamDestroy(cs);
+  }
+  void init() {
+    if (ready) return;
+    MFWQ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      MFWQ_CUDA(cudaMallocHost(&pin[k], CHUNK));
+      MFWQ_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    }
+    MFWQ_CUDA(cudaEventCreateWithFlags(&kdone, cudaEventDisableTiming));
+    ready = true;
+  }
+  void run(Stiffness& S, const double* xh, double* yh, cudaStream_t s) {
+    init();
+    const size_t nin = S.in_elems(), nout = S.out_elems();
+    x.alloc_at_least(nin);
+    y.alloc_at_least(nout);
+    CopyPool& pool = CopyPool::get();
+    const size_t cd = CHUNK / sizeof(double);
+    bool used[2] = {false, false};
+    for (size_t off = 0, k = 0; off < nin; off += cd, ++k) {  // H2D
+      const int sl = int(k & 1);
+      const size_t n = std::min(cd, nin - off);
+      if (used[sl]) MFWQ_CUDA(cudaEventSynchronize(ev[sl]));  // its previous DMA has read it
+      pool.copy(pin[sl], xh + off, n * sizeof(double));
+      MFWQ_CUDA(cudaMemcpyAsync(x.ptr + off, pin[sl], n * sizeof(double), cudaMemcpyHostToDevice, cs));
+      MFWQ_CUDA(cudaEventRecord(ev[sl], cs));
+      used[sl] = true;
+    }
+    MFWQ_CUDA(cudaEventRecord(kdone, cs));
+    MFWQ_CUDA(cudaStreamWaitEvent(s, kdone, 0));
+    S.apply(x.ptr, y.ptr, s);
+    MFWQ_CUDA(cudaEventRecord(kdone, s));
+    MFWQ_CUDA(cudaStreamWaitEvent(cs, kdone, 0));
+    const size_t nch = (nout + cd - 1) / cd;
+    auto issue = [&](size_t k) {
+      const int sl = int(k & 1);
+      const size_t off = k * cd, n = std::min(cd, nout - off);
+      MFWQ_CUDA(cudaMemcpyAsync(pin[sl], y.ptr + off, n * sizeof(double), cudaMemcpyDeviceToHost, cs));
+      MFWQ_CUDA(cudaEventRecord(ev[sl], cs));
+    };
+    for (size_t k = 0; k < std::min<size_t>(2, nch); ++k) issue(k);
+    for (size_t k = 0; k < nch; ++k) {  // D2H
+      const int sl = int(k & 1);
+      const size_t off = k * cd, n = std::min(cd, nout - off);
+      MFWQ_CUDA(cudaEventSynchronize(ev[sl]));
+      pool.copy(yh + off, pin[sl], n * sizeof(double));
+      if (k + 2 < nch) issue(k + 2);
+    }
+  }
+};
+
 struct mfwq_stiffness_s {
   Stiffness op;
   HostPipe pipe;
+  PageablePipe pageable;
 };
 struct mfwq_fd_s { FastDiag fd; };
 struct mfwq_quad_s { Quadrature q; };
@@ -265,6 +409,13 @@ int mfwq_stiffness_apply_host(mfwq_stiffness_t h, const double* x_host, double* 
     MFWQ_CUDA(cudaMemcpyAsync(y_host, P.y[i].ptr, nout * sizeof(double), cudaMemcpyDeviceToHost, P.d2h));
     MFWQ_CUDA(cudaEventRecord(P.read[i], P.d2h));
     P.read_set[i] = true;
+  });
+}
+
+int mfwq_stiffness_apply_pageable(mfwq_stiffness_t h, const double* x_host, double* y_host, void* stream) {
+  return guard([&] {
+    if (x_host == y_host) throw ValueErr("x and y must not be the same buffer");
+    h->pageable.run(h->op, x_host, y_host, (cudaStream_t)stream);
   });
 }
 

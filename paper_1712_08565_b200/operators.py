@@ -201,6 +201,8 @@ class StiffnessOperator:
     def apply(self, v, meter: CostMeter | None = None, out=None):
         if _dev.is_pinned_host(v):
             return self._apply_pinned(v, meter, out)
+        if out is None and isinstance(v, np.ndarray):
+            return self._apply_numpy(v, meter)
         x, host = _dev.to_device(v, self._in_len)
         y = _dev.check_out(out, self._out_len) if out is not None else _dev.empty(self._out_len)
         _lib.check(_lib.lib().mfwq_stiffness_apply(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
@@ -210,6 +212,20 @@ class StiffnessOperator:
         return _dev.back(y, host)
 
     __call__ = apply
+
+    def _apply_numpy(self, v, meter):
+        """numpy in, fresh numpy out (operators.py:185-189 semantics): the native pageable pipeline
+        (mfwq_stiffness_apply_pageable) stages both vectors through pinned chunks on host threads."""
+        x = np.ascontiguousarray(np.asarray(v, dtype=float).ravel())
+        if x.size != self._in_len:
+            raise ValueError(f"expected vector of length {self._in_len}, got {x.size}")
+        y = np.empty(self._out_len)
+        _lib.check(_lib.lib().mfwq_stiffness_apply_pageable(self._h, C.c_void_p(x.ctypes.data),
+                                                            C.c_void_p(y.ctypes.data),
+                                                            C.c_void_p(_dev.stream_ptr())))
+        if meter is not None:
+            meter.add_flops(self.apply_flops)
+        return y
 
     def apply_pipelined(self, v, out=None, meter: CostMeter | None = None):
         """Streaming form of ``apply`` for pinned host tensors: H2D on one side stream, the kernel on
