@@ -146,6 +146,11 @@ int mfwq_stiffness_set_slab(mfwq_stiffness_t h, int e_lo, int e_hi);
 int mfwq_stiffness_slab_info(mfwq_stiffness_t h, int* info6);
 /* select kernel path: 0 = auto (fused), 1 = generic K1 composition, 2 = fused */
 int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path);
+/* deterministic = 1: the fused kernel stores each CTA's output window into its own scratch box and
+   a gather sums the boxes covering every DoF in a fixed order, so applies (and solves built on
+   them) are bitwise reproducible like the reference's; 0 (default): fp64 atomics, whose last
+   bits depend on the arrival order. */
+int mfwq_stiffness_set_deterministic(mfwq_stiffness_t h, int on);
 /* term_mask: bit 3a+b set when C_ab is not identically zero; fused_ok: the rule fits the fused
    kernel's element-blocked structure; kernel_terms: term class the fused kernel runs (3, 5 or 9) */
 int mfwq_stiffness_info(mfwq_stiffness_t h, int* term_mask, int* fused_ok, int* kernel_terms);

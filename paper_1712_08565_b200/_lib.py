@@ -58,6 +58,7 @@ _SIGS = {
     "mfwq_stiffness_host_join": (C.c_int, [C.c_void_p, C.c_void_p]),
     "mfwq_stiffness_apply_pageable": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mfwq_stiffness_set_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "mfwq_stiffness_set_deterministic": (C.c_int, [C.c_void_p, C.c_int]),
     "mfwq_stiffness_set_slab": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "mfwq_stiffness_slab_info": (C.c_int, [C.c_void_p, ip]),
     "mfwq_stiffness_info": (C.c_int, [C.c_void_p, ip, ip, ip]),

@@ -443,6 +443,14 @@ int mfwq_stiffness_set_path(mfwq_stiffness_t h, int path) {
   return guard([&] {
     if (path < 0 || path > 2) throw ValueErr("path must be 0..2");
     h->op.path = path;
+    h->op.pcg_graphs.reset();
+  });
+}
+
+int mfwq_stiffness_set_deterministic(mfwq_stiffness_t h, int on) {
+  return guard([&] {
+    h->op.deterministic = on != 0;
+    h->op.pcg_graphs.reset();  // captured PCG iterations hold the other accumulation scheme
   });
 }
 

@@ -98,6 +98,12 @@ struct Params {
   const double* ztab;
   int xblk_sz, yblk_sz;
   const double* cx;  // on-the-fly mode: C_g(xi1) table [6][m1]
+  // deterministic mode: instead of atomics into y, each CTA stores its output window into its own
+  // box [rows][DM][DM] of det (rows from the chunk's first output row ea3 - 2); f2_gather sums the
+  // boxes covering each DoF in a fixed order.  null = atomics.
+  double* det;
+  long long det_box;
+  int det_dm;
 };
 
 
@@ -583,6 +589,16 @@ __device__ __forceinline__ void fused_body(const Params& prm, const Maps& maps) 
       const int g2 = sInf->day + r, g1 = sInf->dax + c;
       const size_t plane = (size_t)(i3 - prm.y_lo) * n2;
       if (MFWQ_ABLATE == 14 && d0 != 1234.5) continue;
+      if (prm.det) {  // deterministic: this CTA's box, plain stores (every window cell written once)
+        if (r < Dy) {
+          const int dm = prm.det_dm;
+          double* o = prm.det + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * prm.det_box +
+                      ((size_t)(i3 - (sInf->ea3 - 2)) * dm + r) * dm + c;
+          if (c < Dx) o[0] = d0;
+          if (c + 1 < Dx) o[1] = d1;
+        }
+        continue;
+      }
       if (r < Dy && g2 >= 0 && g2 < n2) {
         if (c < Dx && g1 >= 0 && g1 < n1) atomicAdd(&yv[(plane + g2) * n1 + g1], d0);
         if (c + 1 < Dx && g1 + 1 >= 0 && g1 + 1 < n1) atomicAdd(&yv[(plane + g2) * n1 + g1 + 1], d1);
@@ -837,6 +853,42 @@ __global__ void __launch_bounds__(NTHR, Occ<P, KS>::MINB)
   fused_body<P, KS, ZS, OTF>(prm, maps);
 }
 
+// Deterministic mode: y(i3, i2, i1) = the sum, in a fixed (z-chunk, y-tile, x-tile) order, of the
+// window cells of every CTA box covering the DoF; candidate tables per direction: (tile, local
+// index) pairs, -1 padded, KX / KY / KZ per DoF
+struct GatherTabs {
+  const int2* cx;
+  const int2* cy;
+  const int2* cz;
+  int kx, ky, kz;
+};
+static __global__ void __launch_bounds__(256) f2_gather(double* __restrict__ y, const double* __restrict__ det,
+                                                 const __grid_constant__ GatherTabs T, int n1, int n2, int y_lo,
+                                                 int y_hi, int ntx, int nty, long long box, int dm) {
+  const long long n = (long long)(y_hi - y_lo) * n2 * n1;
+  for (long long o = blockIdx.x * 256LL + threadIdx.x; o < n; o += (long long)gridDim.x * 256) {
+    const int i1 = int(o % n1);
+    const long long r = o / n1;
+    const int i2 = int(r % n2), i3 = int(r / n2) + y_lo;
+    double sum = 0.0;
+    for (int a = 0; a < T.kz; ++a) {
+      const int2 z = T.cz[(size_t)i3 * T.kz + a];
+      if (z.x < 0) break;
+      for (int b = 0; b < T.ky; ++b) {
+        const int2 yy = T.cy[(size_t)i2 * T.ky + b];
+        if (yy.x < 0) break;
+        const double* rowp = det + ((size_t)z.x * nty + yy.x) * ntx * box + ((size_t)z.y * dm + yy.y) * dm;
+        for (int c = 0; c < T.kx; ++c) {
+          const int2 xx = T.cx[(size_t)i1 * T.kx + c];
+          if (xx.x < 0) break;
+          sum += rowp[(size_t)xx.x * box + xx.y];
+        }
+      }
+    }
+    y[o] = sum;
+  }
+}
+
 }  // namespace f2
 
 // ---------------------------------------------------------------------------
@@ -855,6 +907,13 @@ struct Fused2Plan {
   const double* maps_for = nullptr;  // coefficient buffer the maps were encoded for
   const double* maps_for_mass = nullptr;  // mass grid the mass maps were encoded for
   f2::Maps maps;  // 16 x 16 x 4 / x 2 boxes: the ZS x 2 planes of a regular step
+  // deterministic mode: candidate tables of the gather, box geometry
+  std::vector<f2::Tile> htiles[3];
+  DevBuf<int2> cand[3];
+  int kc[3] = {0, 0, 0};
+  long long det_box = 0;
+  int det_dm = 0;
+  bool det_ready = false;
 };
 
 #ifndef MFWQ_F2_OTF_UNIT  // plan + tensor maps: defined once (fused2.cu), not in fused2_otf.cu
@@ -968,6 +1027,7 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
       F->q0z.upload(S.dir[2].elem_q0.data(), S.dir[2].elem_q0.size());
     }
     F->ntile[l] = int(t.size());
+    F->htiles[l] = t;
     F->tiles[l].upload(t.data(), t.size());
   }
   if (ok) {  // dense per-tile operand blocks (the band matrices of one tile, zero padded)
@@ -1120,13 +1180,53 @@ static void fill_params(Stiffness& S, Fused2Plan& F, const double* x, double* y,
   prm.cx = S.cx.ptr;
 }
 
+// deterministic mode: the gather's candidate tables (which CTA boxes cover each DoF, in a fixed
+// order) and the box geometry, built once per plan
+static void det_prepare(Stiffness& S, Fused2Plan& F, int dm) {
+  if (F.det_ready && F.det_dm == dm) return;
+  const int p = F.p;
+  auto build = [&](int l, int n, const std::vector<f2::Tile>& t, bool rows) {
+    std::vector<std::vector<int2>> c(n);
+    for (int k = 0; k < (int)t.size(); ++k) {
+      const int lo = t[k].ea - 2, len = rows ? (t[k].eb - t[k].ea) + p + 1 : (t[k].eb - t[k].ea) + p + 1;
+      for (int i = std::max(lo, 0); i < std::min(lo + len, n); ++i) c[i].push_back(make_int2(k, i - lo));
+    }
+    int kmax = 1;
+    for (auto& v : c) kmax = std::max(kmax, (int)v.size());
+    std::vector<int2> flat((size_t)n * kmax, make_int2(-1, -1));
+    for (int i = 0; i < n; ++i)
+      for (size_t a = 0; a < c[i].size(); ++a) flat[(size_t)i * kmax + a] = c[i][a];
+    F.cand[l].upload(flat.data(), flat.size());
+    F.kc[l] = kmax;
+  };
+  build(0, S.dir[0].n, F.htiles[0], false);
+  build(1, S.dir[1].n, F.htiles[1], false);
+  build(2, S.dir[2].n, F.htiles[2], true);
+  F.det_dm = dm;
+  F.det_box = (long long)(F.max_chunk + p + 1) * dm * dm;
+  F.det_ready = true;
+}
+
 // zero w (releasing the fused kernel early), then the fused kernel with programmatic stream
-// serialisation: grid (in-plane tiles, z-chunks, term subsets)
+// serialisation: grid (in-plane tiles, z-chunks, term subsets).  Deterministic mode: no zero pass
+// (every output cell is stored, not added), the fused kernel fully stream-ordered (it reads x in
+// its prologue), then the fixed-order gather into y.
 template <typename K>
-static void launch_chained(Stiffness& S, Fused2Plan& F, K kern, size_t smem, int nsub, const f2::Params& prm,
-                           double* y, cudaStream_t s) {
+static void launch_chained(Stiffness& S, Fused2Plan& F, K kern, size_t smem, int nsub, f2::Params prm,
+                           double* y, cudaStream_t s, int dm = 0) {
   MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  f2_zero_and_chain(y, (long long)S.out_elems(), s);
+  const bool det = S.deterministic && dm > 0;
+  const long long nctas = (long long)F.ntile[0] * F.ntile[1] * F.ntile[2];
+  if (det) {
+    det_prepare(S, F, dm);
+    S.det_scratch.alloc_at_least((size_t)(nctas * F.det_box));
+    prm.det = S.det_scratch.ptr;
+    prm.det_box = F.det_box;
+    prm.det_dm = F.det_dm;
+  } else {
+    prm.det = nullptr;
+    f2_zero_and_chain(y, (long long)S.out_elems(), s);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(F.ntile[0] * F.ntile[1], F.ntile[2], nsub);
   cfg.blockDim = dim3(f2::NTHR);
@@ -1136,10 +1236,19 @@ static void launch_chained(Stiffness& S, Fused2Plan& F, K kern, size_t smem, int
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = det ? 0 : 1;
   MFWQ_CUDA(cudaLaunchKernelEx(&cfg, kern, prm, F.maps));
   note_launch();
   MFWQ_CUDA(cudaGetLastError());
+  if (det) {
+    f2::GatherTabs T{F.cand[0].ptr, F.cand[1].ptr, F.cand[2].ptr, F.kc[0], F.kc[1], F.kc[2]};
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    f2::f2_gather<<<nsm * 8, 256, 0, s>>>(y, prm.det, T, S.dir[0].n, S.dir[1].n, S.y_lo, S.y_hi, F.ntile[0],
+                                          F.ntile[1], F.det_box, F.det_dm);
+    note_launch();
+    MFWQ_CUDA(cudaGetLastError());
+  }
 }
 
 template <int P, int KS, bool OTF>
@@ -1149,7 +1258,8 @@ static void launch2(Stiffness& S, Fused2Plan& F, const double* x, double* y, cud
   if constexpr (!OTF) encode_maps(S, F);
   Params prm;
   fill_params(S, F, x, y, prm);
-  launch_chained(S, F, k_fused<P, KS, ZS, OTF>, Smem<P, KS, ZS, OTF>::bytes(F.qe, F.max_chunk), 1, prm, y, s);
+  launch_chained(S, F, k_fused<P, KS, ZS, OTF>, Smem<P, KS, ZS, OTF>::bytes(F.qe, F.max_chunk), 1, prm, y, s,
+                 Smem<P, KS, ZS, OTF>::DMAX);
 }
 
 template <int P, bool OTF>

@@ -48,6 +48,10 @@ class Stiffness {
   DevBuf<double> pcg_ws;  // PCG work vectors (r, z, p, Ap) + reduction partials, reused across solves
   DevBuf<double> dist_ws;  // slab-distributed PCG workspace of this rank (dist.cu)
   std::shared_ptr<void> pcg_graphs;  // captured PCG iteration bodies (pcg.cu)
+  // deterministic accumulation of the fused matvec: per-CTA output boxes summed in a fixed order
+  // (bitwise reproducible applies) instead of fp64 atomics
+  bool deterministic = false;
+  DevBuf<double> det_scratch;
 
   // on-the-fly coefficients (operators.py:171-183, 207-220): for the analytic maps C depends on
   // xi1 at most, so the kernel reads C(xi1) from a [6][m1] table instead of 6 N_q grids

@@ -265,7 +265,9 @@ void pcg_solve(Stiffness& A, FastDiag* P, const double* b, double* x, long long 
   };
 
   // graphs: built after the first eager solve of this (A, P) pair on this device and host slot
-  auto* G = static_cast<PcgGraphs*>(A.pcg_graphs.get());
+  // a reference keeps the cache alive for this solve even if the operator drops it meanwhile
+  const std::shared_ptr<void> Gkeep = A.pcg_graphs;
+  auto* G = static_cast<PcgGraphs*>(Gkeep.get());
   const bool graphs_ok = !getenv("MFWQ_NO_PCG_GRAPHS");
   const bool use_graphs = graphs_ok && G && G->ready && G->P == P && G->N == N && G->ws == A.pcg_ws.ptr &&
                           G->hslot == hsc && G->device == cur_dev;

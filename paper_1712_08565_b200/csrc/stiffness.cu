@@ -148,6 +148,7 @@ void Stiffness::set_slab(int elo, int ehi) {
   q_lo = z.elem_q0[elo];
   q_hi = z.elem_q0[ehi];
   fused2_plan.reset();
+  pcg_graphs.reset();
   coeffs_ready = false;
 }
 
@@ -259,6 +260,7 @@ __global__ void any_nonzero_kernel(const double* __restrict__ C, size_t n, int* 
 void Stiffness::set_geometry(int kind, const double* A, const double* K9, const double* J_dev,
                              const double* Kfield_dev, cudaStream_t s) {
   otf = false;
+  pcg_graphs.reset();  // captured iterations hold the old coefficient pointers / tensor maps
   cx.release();
   const size_t G = grid_elems();
   coeff.alloc(6 * G);
@@ -351,10 +353,12 @@ void Stiffness::set_on_the_fly(int kind, const double* A, const double* K9, cuda
   otf = true;
   coeffs_ready = true;
   fused2_plan.reset();
+  pcg_graphs.reset();
 }
 
 void Stiffness::set_coeffs(const double* const* grids, cudaStream_t s) {
   otf = false;
+  pcg_graphs.reset();
   cx.release();
   // grids: 6 device arrays, unpadded (m3, m2, m1) -> repack into the padded layout
   const size_t G = grid_elems();

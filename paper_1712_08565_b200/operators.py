@@ -192,6 +192,12 @@ class StiffnessOperator:
         """'auto' | 'generic' | 'fused' kernel path (all on the GPU)."""
         _lib.check(_lib.lib().mfwq_stiffness_set_path(self._h, {"auto": 0, "generic": 1, "fused": 2}[path]))
 
+    def set_deterministic(self, enabled: bool = True):
+        """Bitwise reproducible applies: the fused kernel's overlapping output windows are summed
+        in a fixed order instead of by fp64 atomics (the reference's numpy apply is deterministic)."""
+        self.deterministic = bool(enabled)
+        _lib.check(_lib.lib().mfwq_stiffness_set_deterministic(self._h, int(self.deterministic)))
+
     def info(self):
         tm, ok, nt = C.c_int(), C.c_int(), C.c_int()
         _lib.check(_lib.lib().mfwq_stiffness_info(self._h, C.byref(tm), C.byref(ok), C.byref(nt)))

@@ -107,6 +107,12 @@ def test_cfg3_pcg_deterministic_iterations():
     ref = us[0]
     worst = max(float(torch.linalg.vector_norm(u - ref) / torch.linalg.vector_norm(ref)) for u in us[1:])
     assert worst <= 1e-12, worst
+    # deterministic accumulation (set_deterministic): the solves agree bit for bit
+    A.set_deterministic(True)
+    u1, r1 = M.cg(A.apply, b, P.apply, tol=1e-8)
+    u2, r2 = M.cg(A.apply, b, P.apply, tol=1e-8)
+    assert r1.iterations == r2.iterations == its[0] and torch.equal(u1, u2) and r1.residuals == r2.residuals
+    assert_matches(u1, "cfg3_u", U_TOL)
 
 
 def test_fd_round_trip_cfg3_size():

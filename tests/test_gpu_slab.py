@@ -136,3 +136,25 @@ def test_distributed_pcg_single_rank_nccl():
         assert relerr(u.cpu().numpy(), u1.cpu().numpy()) <= 1e-9
     finally:
         dist.destroy_process_group()
+
+
+def test_slab_windows_sum_to_global_deterministic():
+    """Deterministic mode on slab handles (output window rows [y_lo, y_hi))."""
+    p, n_el, world = 4, 16, 3
+    space = M.tensor_space(p, n_el)
+    rule = M.build_tensor_rule(space)
+    geom = M.quarter_ring_map()
+    A = M.setup_stiffness(space, rule, geom)
+    A.set_deterministic(True)
+    plane = A.n[0] * A.n[1]
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(A.n_dofs)).cuda()
+    ref = A.apply(x)
+    part = SlabPartition(n_el, p, A.n[2], world).validate()
+    y = torch.zeros_like(ref)
+    for r in range(world):
+        op = M.StiffnessOperator(space, rule, geom, _slab=part.elements(r))
+        op.set_deterministic(True)
+        vlo, vhi = part.in_window(r)
+        ylo, yhi = part.out_window(r)
+        y[ylo * plane:yhi * plane] += op.apply(x[vlo * plane:vhi * plane])
+    assert relerr(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
