@@ -52,19 +52,22 @@ class CopyPool {
       return;
     }
     const size_t per = (bytes / parts + 63) & ~size_t(63);
+    size_t mine = 0;  // tasks of this call (other host threads may be copying concurrently)
     {
       std::unique_lock<std::mutex> lk(m_);
       for (int k = 1; k < parts; ++k) {
         const size_t o = per * k;
-        if (o < bytes) tasks_.push_back({static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
-                                         std::min(per, bytes - o)});
+        if (o < bytes) {
+          tasks_.push_back({static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                            std::min(per, bytes - o), &mine});
+          ++mine;
+        }
       }
-      pending_ += tasks_.size();
     }
     cv_.notify_all();
     std::memcpy(dst, src, std::min(per, bytes));
     std::unique_lock<std::mutex> lk(m_);
-    done_.wait(lk, [&] { return pending_ == 0; });
+    done_.wait(lk, [&] { return mine == 0; });
   }
   ~CopyPool() {
     {
@@ -76,7 +79,7 @@ class CopyPool {
   }
 
  private:
-  struct Task { char* dst; const char* src; size_t n; };
+  struct Task { char* dst; const char* src; size_t n; size_t* left; };  // left: the caller's count
   CopyPool() {
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
     const int n = int(std::min(7u, hw / 2));  // + the caller
@@ -94,12 +97,11 @@ class CopyPool {
       }
       std::memcpy(t.dst, t.src, t.n);
       std::lock_guard<std::mutex> lk(m_);
-      if (--pending_ == 0) done_.notify_all();
+      if (--*t.left == 0) done_.notify_all();
     }
   }
   std::vector<std::thread> workers_;
   std::vector<Task> tasks_;
-  size_t pending_ = 0;
   bool stop_ = false;
   std::mutex m_;
   std::condition_variable cv_, done_;

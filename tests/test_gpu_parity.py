@@ -304,3 +304,32 @@ def test_deterministic_matvec_is_bitwise_reproducible(p, n_el, kind):
     y2 = A.apply(x).clone()
     assert torch.equal(y1, y2)
     assert relerr(y1.cpu().numpy(), ya.cpu().numpy()) <= 1e-14
+
+
+def test_numpy_apply_pageable_pipeline_multi_chunk_and_threads():
+    """A.apply(np.ndarray): the native pageable pipeline (pinned chunk slots, host copy pool) over
+    several chunks, from two host threads at once, equals the device-tensor apply."""
+    import threading
+
+    import torch
+    space = M.tensor_space(3, 80)  # 531,441 DoFs: more than one 4 MB staging chunk each way
+    rule = M.build_tensor_rule(space)
+    ops = [M.setup_stiffness(space, rule, M.quarter_ring_map()) for _ in range(2)]
+    for A in ops:
+        A.set_deterministic(True)  # bitwise comparable
+    xs = [np.random.default_rng(s).standard_normal(space.n_dofs) for s in range(2)]
+    refs = [A.apply(torch.from_numpy(x).cuda()).cpu().numpy() for A, x in zip(ops, xs)]
+    out = [None, None]
+
+    def run(i):
+        torch.cuda.set_device(0)
+        for _ in range(3):
+            out[i] = ops[i].apply(xs[i])
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(2):
+        assert isinstance(out[i], np.ndarray) and np.array_equal(out[i], refs[i])
