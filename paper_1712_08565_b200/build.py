@@ -35,7 +35,7 @@ def _nccl_include():
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()] + \
     os.environ.get("MFWQ_NVCC_EXTRA", "").split()
-SOURCES = ["rule1d.cpp", "stiffness.cu", "fused2.cu", "fused2_otf.cu", "fd.cu", "modal_gemm.cu", "pcg.cu",
+SOURCES = ["rule1d.cpp", "stiffness.cu", "fused2.cu", "fused2_otf.cu", "fused3.cu", "fd.cu", "modal_gemm.cu", "pcg.cu",
            "bicgstab.cu", "quadrature.cu", "dist.cu", "capi.cu"]
 LIBS = ["-lcusolver", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64"]
 

@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "ops.h"
@@ -894,6 +895,17 @@ static __global__ void __launch_bounds__(256) f2_gather(double* __restrict__ y, 
 // ---------------------------------------------------------------------------
 // host: plan (element-blocked tables, tiles, tensor maps), dispatch
 // ---------------------------------------------------------------------------
+// The warp-specialised kernel (fused3.cu, one CTA per SM) runs the cases it measured faster in
+// (tools/f3_sweep.sh, profiles/f3_sweep_r02.txt): the three-term kernel from p = 2 (stored and on the
+// fly), the five-term kernel at p = 1, 2, 4.  MFWQ_F3=0 keeps the phased kernel everywhere, MFWQ_F3=2
+// takes the warp-specialised one wherever it exists (p <= 6).
+inline bool f3_wanted(int p, int ks) {
+  static const int on = [] { const char* e = getenv("MFWQ_F3"); return e ? atoi(e) : 1; }();
+  if (!on || p < 1 || p > 6 || (ks != 0x111 && ks != 0x11B)) return false;
+  if (on == 2) return true;
+  return ks == 0x111 ? p >= 2 : (p == 1 || p == 2 || p == 4);
+}
+
 struct Fused2Plan {
   bool ok = false;
   int p = 0;
@@ -1002,7 +1014,7 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
       const long long inplane = (long long)F->ntile[0] * F->ntile[1];
       const int mask = S.term_mask();
       const int ks = (mask & ~0x111) == 0 ? 0x111 : ((mask & ~0x11B) == 0 ? 0x11B : 0x1FF);
-      const int occ = f2::occ_for(p, ks);
+      const int occ = f3_wanted(p, ks) ? 1 : f2::occ_for(p, ks);
       int dev = 0, nsm = 148;
       if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const long long slots = (long long)occ * nsm;
@@ -1213,7 +1225,7 @@ static void det_prepare(Stiffness& S, Fused2Plan& F, int dm) {
 // its prologue), then the fixed-order gather into y.
 template <typename K>
 static void launch_chained(Stiffness& S, Fused2Plan& F, K kern, size_t smem, int nsub, f2::Params prm,
-                           double* y, cudaStream_t s, int dm = 0) {
+                           double* y, cudaStream_t s, int dm = 0, int nthr = f2::NTHR) {
   MFWQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const bool det = S.deterministic && dm > 0;
   const long long nctas = (long long)F.ntile[0] * F.ntile[1] * F.ntile[2];
@@ -1229,7 +1241,7 @@ static void launch_chained(Stiffness& S, Fused2Plan& F, K kern, size_t smem, int
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(F.ntile[0] * F.ntile[1], F.ntile[2], nsub);
-  cfg.blockDim = dim3(f2::NTHR);
+  cfg.blockDim = dim3(nthr);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1296,10 +1308,12 @@ static bool dispatch_p(Stiffness& S, Fused2Plan& F, const double* x, double* y, 
 
 #ifndef MFWQ_F2_OTF_UNIT
 bool fused2_apply_otf(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s);  // fused2_otf.cu
+bool fused3_apply(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s);      // fused3.cu
 
 bool fused2_apply(Stiffness& S, const double* x, double* y, cudaStream_t s) {
   Fused2Plan* F = fused2_plan(S);
   if (!F->ok) return false;
+  if (fused3_apply(S, *F, x, y, s)) return true;  // warp-specialised kernel (fused3.cu) where it applies
   if (S.otf) return fused2_apply_otf(S, *F, x, y, s);
   return dispatch_p<false>(S, *F, x, y, s);
 }
@@ -1337,7 +1351,7 @@ void Stiffness::apply_fused(const double* x, double* y, cudaStream_t s) {
   if (is_slab()) throw NotImplErr("slab operators need the element-blocked fused kernel (p <= 10, n_el >= 2)");
   apply_generic(x, y, s);  // rule outside the element-blocked structure: composed K1 path (still GPU)
 }
-#else
+#elif !defined(MFWQ_F3_UNIT)
 bool fused2_apply_otf(Stiffness& S, Fused2Plan& F, const double* x, double* y, cudaStream_t s) {
   return dispatch_p<true>(S, F, x, y, s);
 }
