@@ -1,4 +1,4 @@
-"""Write profiles/traffic.json from an ncu report holding one k_fused launch per sweep degree.
+"""Write profiles/traffic.json from an ncu report holding one fused-matvec launch (k_fused / k_ws) per sweep degree.
     python tools/make_traffic.py gpurun_out/sweep.ncu-rep "<source description>"
 Per degree: DRAM bytes (read + write) and the ncu (serialised, cold-cache) duration."""
 import csv
@@ -19,7 +19,8 @@ col = {h: i for i, h in enumerate(hdr)}
 scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1, 'us': 1, 'msecond': 1e3, 'ms': 1e3}
 per = {}
 for r in rows[2:]:
-    m = re.search(r'k_fused<(\d+), (\d+), (\d+), (?:0|false)>', r[col['Kernel Name']])
+    m = (re.search(r'k_fused<(\d+), (\d+), (\d+), (?:0|false)>', r[col['Kernel Name']]) or
+         re.search(r'k_ws<(\d+), (\d+), (?:0|false)>', r[col['Kernel Name']]))
     if not m:
         continue
     v = lambda k: float(r[col[k]].replace(',', '')) * scale[units[col[k]]]
