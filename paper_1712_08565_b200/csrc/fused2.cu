@@ -1097,7 +1097,9 @@ static Fused2Plan* fused2_plan(Stiffness& S) {
   }
   F->qe = maxe;
   F->p = p;
-  F->ok = ok && maxe <= f2::TQ;
+  // the v-window fetch packs (in-plane DoF offset << 10 | window cell) into an int
+  const bool plane_fits = (long long)S.dir[0].n * S.dir[1].n < (1ll << 21);
+  F->ok = ok && maxe <= f2::TQ && plane_fits;
   return F;
 }
 

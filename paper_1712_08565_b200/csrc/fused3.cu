@@ -25,7 +25,8 @@
 
 #ifndef MFWQ_F3_ABL
 #define MFWQ_F3_ABL 0  // timing experiments only (wrong results): 1 = z rows from immediates, 2 = Bx from immediates,
-                       // 4 = helpers skip their DMMAs, 8 = column warps skip their arithmetic
+                       // 4 = helpers skip their DMMAs, 8 = column warps skip their arithmetic,
+                       // 16 = column warps alone: helpers exit after the setup, no ring waits or arrivals
 #endif
 namespace mfwq {
 namespace f3 {
@@ -58,6 +59,7 @@ enum {
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  if (MFWQ_F3_ABL & 16) return;
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_acq(uint64_t* b, unsigned parity) {
@@ -77,7 +79,7 @@ __device__ __forceinline__ void mbar_wait_acq(uint64_t* b, unsigned parity) {
 #define SECTR plast = clock64();
 #define PROF3_DUMP(name) if (blockIdx.x == 40 && blockIdx.y == 0 && lane == 0) printf("F3PROF %s w%d total %lld wait0 %lld wait1 %lld wait2 %lld | s3 %lld s4 %lld s5 %lld s6 %lld\n", name, warp, clock64() - pstart, pw[0], pw[1], pw[2], pw[3], pw[4], pw[5], pw[6]);
 #else
-#define WAITP(slot, b, par) mbar_wait_acq(b, par)
+#define WAITP(slot, b, par) { if (!(MFWQ_F3_ABL & 16)) mbar_wait_acq(b, par); }
 #define PROF3_DECL
 #define SECT(slot)
 #define SECT0
@@ -205,6 +207,7 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
 #ifndef MFWQ_F3_NOSETREG
   if (!colw) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_HELP));
 #endif
+  if ((MFWQ_F3_ABL & 16) && !colw) return;
   if (colw) {
     // =========================== column warps ===========================
 #ifndef MFWQ_F3_NOSETREG
