@@ -897,13 +897,13 @@ static __global__ void __launch_bounds__(256) f2_gather(double* __restrict__ y, 
 // ---------------------------------------------------------------------------
 // The warp-specialised kernel (fused3.cu, one CTA per SM) runs the cases it measured faster in
 // (tools/f3_sweep.sh, profiles/f3_sweep_r02.txt): the three-term kernel from p = 2 (stored and on the
-// fly), the five-term kernel at p = 1, 2, 4.  MFWQ_F3=0 keeps the phased kernel everywhere, MFWQ_F3=2
+// fly), the five-term kernel at p = 1, 2, 4, 6.  MFWQ_F3=0 keeps the phased kernel everywhere, MFWQ_F3=2
 // takes the warp-specialised one wherever it exists (p <= 6).
 inline bool f3_wanted(int p, int ks) {
   static const int on = [] { const char* e = getenv("MFWQ_F3"); return e ? atoi(e) : 1; }();
   if (!on || p < 1 || p > 6 || (ks != 0x111 && ks != 0x11B)) return false;
   if (on == 2) return true;
-  return ks == 0x111 ? p >= 2 : (p == 1 || p == 2 || p == 4);
+  return ks == 0x111 ? p >= 2 : (p == 1 || p == 2 || p == 4 || p == 6);
 }
 
 struct Fused2Plan {

@@ -18,7 +18,8 @@
 //   warps 14,15 W y-contraction (DMMA, Wy band fragments stationary) and the fp64 atomics into w.
 //
 // Rings (full / empty mbarriers per stage): V loader -> B y;  A B y -> columns;  C loader -> columns;
-// T columns -> W x;  S W x -> W y.  No CTA barrier after the setup.
+// T columns -> W x;  S W x -> W y.  The column warps signal one barrier per step ("row retired"), which
+// W x, the loader and B y all wait on.  No CTA barrier after the setup.
 #define MFWQ_F2_OTF_UNIT 1
 #define MFWQ_F3_UNIT 1
 #include "fused2.cu"
@@ -53,9 +54,15 @@ constexpr int H_WX = 0, H_BY = 2, H_LOAD = 4, H_WY = 6;
 #define MFWQ_F3_ST 2
 #endif
 constexpr int SV = MFWQ_F3_SV, SA = 4, SC = MFWQ_F3_SC, ST = MFWQ_F3_ST, SS = MFWQ_F3_ST;  // ring depths (powers of two)
+// "Row j retired" (B_FT, one arrival per column warp) is the only barrier the column warps signal per
+// step: W x waits on it for the row, the loader for the coefficient stage of element j (free again)
+// and B y for the A plane element j consumed.  It has NFT barriers (row j -> j mod NFT) although the
+// T data ring has ST slots; no waiter is ever NFT rows behind the column warps.
+constexpr int NFT = 4;
+static_assert(SC <= NFT && SA <= NFT && ST <= NFT, "a waiter must see the phase it waits for");
 enum {
-  B_FV = 0, B_EV = B_FV + SV, B_FA = B_EV + SV, B_EA = B_FA + SA, B_FC = B_EA + SA, B_EC = B_FC + SC,
-  B_FT = B_EC + SC, B_ET = B_FT + ST, B_FS = B_ET + ST, B_ES = B_FS + SS, NBAR = B_ES + SS
+  B_FV = 0, B_EV = B_FV + SV, B_FA = B_EV + SV, B_EA = B_FA + SA, B_FC = B_EA + SA,
+  B_FT = B_FC + SC, B_ET = B_FT + NFT, B_FS = B_ET + ST, B_ES = B_FS + SS, NBAR = B_ES + SS
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -188,8 +195,9 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
     if (tid == 0) {
       for (int i = 0; i < SV; ++i) { mbar_init(&bar[B_FV + i], 32); mbar_init(&bar[B_EV + i], 2); }
       for (int i = 0; i < SA; ++i) { mbar_init(&bar[B_FA + i], 2); mbar_init(&bar[B_EA + i], 8); }
-      for (int i = 0; i < SC; ++i) { mbar_init(&bar[B_FC + i], 1); mbar_init(&bar[B_EC + i], 8); }
-      for (int i = 0; i < ST; ++i) { mbar_init(&bar[B_FT + i], 8); mbar_init(&bar[B_ET + i], 2); }
+      for (int i = 0; i < SC; ++i) mbar_init(&bar[B_FC + i], 1);
+      for (int i = 0; i < NFT; ++i) mbar_init(&bar[B_FT + i], 8);
+      for (int i = 0; i < ST; ++i) mbar_init(&bar[B_ET + i], 2);
       for (int i = 0; i < SS; ++i) { mbar_init(&bar[B_FS + i], 2); mbar_init(&bar[B_ES + i], 2); }
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
@@ -376,12 +384,6 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
             zpart(Uc, std::false_type{}, nq, qa, zr, nullptr);
           }
           SECT(4)
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&bar[B_EC + sc]);
-            if (more) mbar_arrive(&bar[B_EA + san]);
-          }
-          SECT(5)
         }
         SECT0
         const int st = j & (ST - 1);
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
           o[t * TQ * PK] = acc[t][u];
           acc[t][u] = 0.0;
         }
-        warp_arrive(&bar[B_FT + st], lane);
+        warp_arrive(&bar[B_FT + (j & (NFT - 1))], lane);  // row j retired: also frees its coefficient stage and A plane
         SECT(6)
       });
     }
@@ -423,7 +425,7 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
     PROF3_DECL
     for (int j = 0; j < nrows; ++j) {
       const int st = j % ST;
-      WAITP(0, &bar[B_FT + st], (j / ST) & 1);
+      WAITP(0, &bar[B_FT + (j & (NFT - 1))], (j / NFT) & 1);
       double d[NY][2][2];
 #pragma unroll
       for (int ys = 0; ys < NY; ++ys)
@@ -503,7 +505,11 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
           for (int mt = 0; mt < 2; ++mt)
             if (!(MFWQ_F3_ABL & 4) && (nzb & (1u << (mt * KB + ks)))) dmma(d[bs][mt][0], d[bs][mt][1], a[bs][mt][ks], bv[ks]);
       const int sa = k % SA;
-      WAITP(1, &bar[B_EA + sa], ((k / SA) & 1) ^ 1);
+      if (k >= SA) {  // the plane that held this stage: x-contracted in the prologue (planes 0 .. P), else by element kp - P - 1
+        const int kp = k - SA;
+        if (kp <= P) { WAITP(1, &bar[B_EA + (kp & (SA - 1))], (kp / SA) & 1); }
+        else { const int r = kp - P - 1; WAITP(1, &bar[B_FT + (r & (NFT - 1))], (r / NFT) & 1); }
+      }
 #pragma unroll
       for (int bs = 0; bs < NBY; ++bs) {
         const int b = NBY == 2 ? bs : (kA0 ? 0 : 1);
@@ -542,7 +548,7 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
       SECT(4)
       if (it >= P && lane == 0) {  // the stage of element it - P: z rows, coefficient boxes of a regular element
         const int el = it - P, sc = el % SC;
-        WAITP(1, &bar[B_EC + sc], ((el / SC) & 1) ^ 1);
+        if (el >= SC) { const int r = el - SC; WAITP(1, &bar[B_FT + (r & (NFT - 1))], (r / NFT) & 1); }
         SECTR
         const int qa = sQ0[el], nq = sQ0[el + 1] - qa;
         const bool tma = !OTF && nq == 2;
