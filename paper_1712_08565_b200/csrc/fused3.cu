@@ -93,6 +93,20 @@ __device__ __forceinline__ void mbar_wait_acq(uint64_t* b, unsigned parity) {
 #define SECTR
 #define PROF3_DUMP(name)
 #endif
+// coefficient boxes are read once: evict-first in L2, so the stream does not push v and w out
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_3d_hint(double* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], "
+      "[%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
@@ -531,6 +545,7 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
       const bool ok = e < Dy * Dx && g2 >= 0 && g2 < prm.n2 && g1 >= 0 && g1 < prm.n1;
       code[j] = ok ? ((g2 * prm.n1 + g1) << 10) | (r * PV + (c ^ swz(r))) : -1;
     }
+    const uint64_t pol = l2_evict_first_policy();
     PROF3_DECL
     for (int it = 0; it < nplanes; ++it) {
       const int sv = it % SV;
@@ -558,8 +573,8 @@ __global__ void __launch_bounds__(NTHR3, 1) k_ws(const __grid_constant__ Params 
 #pragma unroll
           for (int h = 0; h < NGRID; ++h)
             if (grid_used<KS>(h))
-              tma_load_3d(sC + sc * L::CSZ + grid_slot<KS>(h) * 2 * 256, &maps.m[NGRID + h], tx.q0, ty.q0, qa - prm.qzb,
-                          &bar[B_FC + sc]);
+              tma_load_3d_hint(sC + sc * L::CSZ + grid_slot<KS>(h) * 2 * 256, &maps.m[NGRID + h], tx.q0, ty.q0, qa - prm.qzb,
+                               &bar[B_FC + sc], pol);
         }
         SECT(5)
       }
